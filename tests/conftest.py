@@ -1,0 +1,45 @@
+"""Shared fixtures.  GPU tests carry @pytest.mark.gpu and run on a B200 via gpurun."""
+
+import json
+import os
+import sys
+
+import numpy as np
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+GOLDEN = os.path.join(ROOT, "tests", "golden")
+
+
+def pytest_configure(config):
+    config.addinivalue_line("markers", "gpu: needs a CUDA device (B200); run with -m gpu")
+
+
+@pytest.fixture(scope="session")
+def manifest():
+    with open(os.path.join(GOLDEN, "manifest.json")) as f:
+        return json.load(f)
+
+
+def load_golden(name_or_file):
+    from paper_2302_09005_b200 import mesh
+
+    fname = name_or_file if name_or_file.endswith(".fvb") else name_or_file + ".fvb"
+    return mesh.load_batch(os.path.join(GOLDEN, fname))
+
+
+def assert_bits_equal(a, b, what=""):
+    """Bitwise equality of float64 arrays; NaN positions must coincide (payloads may differ)."""
+    a = np.ascontiguousarray(a, dtype=np.float64)
+    b = np.ascontiguousarray(b, dtype=np.float64)
+    assert a.shape == b.shape, (what, a.shape, b.shape)
+    nan_a, nan_b = np.isnan(a), np.isnan(b)
+    assert np.array_equal(nan_a, nan_b), f"{what}: NaN positions differ"
+    same = (a.view(np.uint64) == b.view(np.uint64)) | nan_a
+    if not np.all(same):
+        idx = np.argwhere(~same)[:5]
+        details = [(tuple(i), a[tuple(i)], b[tuple(i)]) for i in idx]
+        raise AssertionError(f"{what}: {int((~same).sum())} elements differ bitwise, e.g. {details}")
