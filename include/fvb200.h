@@ -1,0 +1,132 @@
+/*
+ * fvb200.h -- C ABI of libfvb200.so, the B200 (sm_100a) batched Rusanov
+ * finite-volume patch update.
+ *
+ * Drop-in boundary for the reference package `fvbatch` (arXiv 2302.09005
+ * clean-room re-implementation, /root/reference/pkg).  Each entry point names
+ * the reference interface it replaces.  Plain C types only: device pointers
+ * are raw `double*` / `uint32_t*`, streams are `cudaStream_t` passed as
+ * `void*` (NULL = legacy default stream).  The library allocates no device
+ * memory per call; callers own every buffer.
+ *
+ * Array layouts (mesh.py:6-7, :119-134):
+ *   AoS (layout 0): qin[(patch*V + vol)*S + u], qout[(patch*I + vol)*S + u]
+ *   SoA (layout 1): qin[(u*N + patch)*V + vol], qout[(u*N + patch)*I + vol]
+ *   V = (p+2)^d haloed volumes, I = p^d interior volumes, S = d+2 unknowns,
+ *   volumes linearised x fastest, [z][y][x].
+ *
+ * Return codes map to the reference's exceptions (errors.py):
+ *   FVB_OK 0, FVB_ERR_CONTRACT 1 -> ContractViolationError,
+ *   FVB_ERR_NONPHYSICAL 2 -> NonPhysicalStateError (locate with fvb_locate),
+ *   FVB_ERR_CUDA 3 -> device failure (fvb_strerror / cudaGetLastError text).
+ */
+#ifndef FVB200_H
+#define FVB200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define FVB_OK 0
+#define FVB_ERR_CONTRACT 1
+#define FVB_ERR_NONPHYSICAL 2
+#define FVB_ERR_CUDA 3
+
+/* kernel selector for fvb_update / fvb_update_host */
+#define FVB_KERNEL_AUTO 0     /* fused p=16 kernel when the shape has one, else generic */
+#define FVB_KERNEL_GENERIC 1  /* any d, p */
+#define FVB_KERNEL_FUSED 2    /* d in {2,3}, p == 16 only */
+
+typedef struct fvb_spec {
+  int32_t dim;       /* PatchSpec.dimensions (mesh.py:29), 2 or 3 */
+  int32_t p;         /* PatchSpec.volumes_per_axis (mesh.py:30) */
+  int32_t unknowns;  /* PatchSpec.unknowns; must be dim + 2 (Euler, pde.py:121) */
+  int32_t layout;    /* 0 = AoS (PatchBatch), 1 = SoA (LayoutEnumerator SOA) */
+  int64_t n_patches; /* PatchBatch.n_patches */
+  double gamma;      /* EulerParameters.gamma (pde.py:19-30) */
+} fvb_spec;
+
+/* Per-(patch, box) diagnostics of the face-box volumes (see fvb_locate). */
+typedef struct fvb_boxinfo {
+  int64_t trig_rho;     /* any rho <= 0           (pde.py:36-38) */
+  int64_t trig_p;       /* any p < 0              (pde.py:66-68) */
+  int64_t first_nonpos; /* first box index with !(rho > 0), -1 if none   (vectorized.py:86) */
+  int64_t first_badpl;  /* first box index with !(E - |j|^2/(2 rho) >= 0), -1 if none (vectorized.py:88-90) */
+} fvb_boxinfo;
+
+int fvb_version(void);
+const char* fvb_strerror(int code);
+
+/* Which kernel FVB_KERNEL_AUTO resolves to for this spec (1 generic, 2 fused). */
+int fvb_select_kernel(const fvb_spec* spec);
+
+/* One forward-Euler Rusanov step for every patch, device-resident.
+ * Replaces fvbatch.kernel.update_patch_batch (kernel/__init__.py:114-140) and
+ * the engine it dispatches to (vectorized.run, vectorized.py:246-288).
+ *   qin        [N*V*S]  haloed input, read only
+ *   qout       [N*I*S]  interior output (written)
+ *   cell_size  [N*dim]  only cell_size[patch*dim + 0] is read (vectorized.py:169)
+ *   dt         [N]      per-patch time step, must be >= 0 (checked by the host)
+ *   max_eig    [N]      per-patch max directional wave speed (written, vectorized.py:226-231)
+ *   status     [1]      device word, ORed with 1 when a face-box volume has rho <= 0 or
+ *                       p < 0; the caller zeroes it (or passes zero_status = 1).
+ * Asynchronous on `stream`.  Returns FVB_OK or FVB_ERR_CONTRACT / FVB_ERR_CUDA. */
+int fvb_update(const fvb_spec* spec, const double* qin, double* qout, const double* cell_size,
+               const double* dt, double* max_eig, uint32_t* status, int kernel, int zero_status,
+               void* stream);
+
+/* Same step from HOST arrays (the reference's calling convention, numpy
+ * buffers): chunked, double-buffered H2D copy -> update -> D2H copy, with
+ * copies and kernels overlapped on the given stream plus one internal copy
+ * stream per direction.  `workspace` is device memory of at least
+ * fvb_update_host_workspace(spec, chunk_patches) bytes.  Synchronous; returns
+ * FVB_ERR_NONPHYSICAL when the status word was raised (then call fvb_locate). */
+size_t fvb_update_host_workspace(const fvb_spec* spec, int64_t chunk_patches);
+int fvb_update_host(const fvb_spec* spec, const double* qin_host, double* qout_host,
+                    const double* cell_size_host, const double* dt_host, double* max_eig_host,
+                    void* workspace, size_t workspace_bytes, int64_t chunk_patches, int kernel,
+                    void* stream);
+
+/* Error path: per-(patch, box) diagnostics for the 2*dim+1 boxes of
+ * vectorized._plan (vectorized.py:42-53), box-linear index in C order over the
+ * box's (z, y, x) extents.  info has N*(2*dim+1) entries (device). */
+int fvb_locate(const fvb_spec* spec, const double* qin, fvb_boxinfo* info, void* stream);
+
+/* AoS <-> SoA batch packer (LayoutEnumerator AOS/SOA maps, mesh.py:127-130).
+ * interior = 0 packs haloed QIn-shaped arrays, 1 interior QOut-shaped arrays. */
+int fvb_pack(const fvb_spec* spec, const double* aos, double* soa, int interior, void* stream);
+int fvb_unpack(const fvb_spec* spec, const double* soa, double* aos, int interior, void* stream);
+
+/* Global wave speed and CFL step: gmax = max over patches
+ * of max_eig (NaN propagates), then dt = (cfl*dx)/gmax written to dt_scalar
+ * and broadcast to dt_patches[N] (either may be NULL).  For multi-GPU runs
+ * call with do_dt = 0, all-reduce gmax (MAX) across ranks, then fvb_set_dt. */
+int fvb_reduce_dt(const double* max_eig, int64_t n, double cfl, double dx, double* gmax,
+                  double* dt_scalar, double* dt_patches, int do_dt, void* stream);
+int fvb_set_dt(const double* gmax, double cfl, double dx, double* dt_scalar, double* dt_patches,
+               int64_t n, void* stream);
+
+/* First-step wave-speed pre-pass: per-patch max over interior
+ * volumes and directions of |u_n| + c, no update. max_eig must be zeroed. */
+int fvb_patch_max_eig(const fvb_spec* spec, const double* qin, double* max_eig, uint32_t* status,
+                      void* stream);
+
+/* Closure probe: wave speeds lam[i*dim + k], fluxes flux[(i*dim + k)*S + u],
+ * pressure[i] and bad[i] (0 ok, 1 rho <= 0, 2 p < 0) of n AoS states -- the
+ * device twin of the Euler callbacks (euler_pressure / euler_flux /
+ * euler_max_eigenvalue, pde.py:33-70, bound by make_euler_pde, :115-119).
+ * pressure and bad may be NULL. */
+int fvb_probe(int dim, double gamma, const double* states, int64_t n, double* lam, double* flux,
+              double* pressure, uint8_t* bad, void* stream);
+
+/* Self-test: shared-reciprocal division vs IEEE division for n operand pairs. */
+int fvb_selftest_div(const double* a, const double* b, double* out_shared, double* out_ieee,
+                     int64_t n, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FVB200_H */

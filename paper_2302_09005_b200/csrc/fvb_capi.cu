@@ -1,0 +1,270 @@
+// fvb_capi.cu -- the extern "C" boundary of libfvb200.so (declared in include/fvb200.h).
+//
+// Thin, allocation-free argument checking and dispatch on top of the kernel
+// launchers, plus the host-buffer pipeline of fvb_update_host (chunked H2D ->
+// update -> D2H overlapped across three streams).
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <cstdio>
+#include <cstring>
+
+#include "../../include/fvb200.h"
+#include "fvb_kernels.h"
+#include "fvb_layout.cuh"
+
+namespace {
+
+thread_local char g_last_error[256] = "";
+
+int set_cuda_error(cudaError_t e, const char* where) {
+  snprintf(g_last_error, sizeof(g_last_error), "%s: %s", where, cudaGetErrorString(e));
+  return FVB_ERR_CUDA;
+}
+
+int set_contract(const char* msg) {
+  snprintf(g_last_error, sizeof(g_last_error), "%s", msg);
+  return FVB_ERR_CONTRACT;
+}
+
+int check_spec(const fvb_spec* s) {
+  if (!s) return set_contract("null spec");
+  if (s->dim != 2 && s->dim != 3) return set_contract("dimensions must be 2 or 3");
+  if (s->p < 1) return set_contract("volumes_per_axis must be >= 1");
+  if (s->unknowns != s->dim + 2) return set_contract("Euler needs dim + 2 unknowns");
+  if (s->layout != 0 && s->layout != 1) return set_contract("layout must be 0 (AoS) or 1 (SoA)");
+  if (s->n_patches < 0) return set_contract("negative patch count");
+  if (!(s->gamma > 1.0)) return set_contract("gamma must exceed 1");
+  return FVB_OK;
+}
+
+inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+int resolve_kernel(const fvb_spec* s, int kernel) {
+  if (kernel == FVB_KERNEL_AUTO)
+    return fvb_fused16_supported(s->dim, s->p, s->layout) ? FVB_KERNEL_FUSED : FVB_KERNEL_GENERIC;
+  return kernel;
+}
+
+}  // namespace
+
+extern "C" {
+
+int fvb_version(void) { return 1; }
+
+const char* fvb_strerror(int code) {
+  if (code == FVB_OK) return "ok";
+  if (g_last_error[0]) return g_last_error;
+  switch (code) {
+    case FVB_ERR_CONTRACT: return "contract violation";
+    case FVB_ERR_NONPHYSICAL: return "non-physical state";
+    case FVB_ERR_CUDA: return "CUDA error";
+    default: return "unknown error";
+  }
+}
+
+int fvb_select_kernel(const fvb_spec* spec) {
+  int rc = check_spec(spec);
+  if (rc) return -rc;
+  return resolve_kernel(spec, FVB_KERNEL_AUTO);
+}
+
+int fvb_update(const fvb_spec* spec, const double* qin, double* qout, const double* cell_size, const double* dt,
+               double* max_eig, uint32_t* status, int kernel, int zero_status, void* stream) {
+  int rc = check_spec(spec);
+  if (rc) return rc;
+  if (spec->n_patches == 0) return FVB_OK;   // kernel/__init__.py:123-124
+  if (!qin || !qout || !cell_size || !dt || !max_eig || !status) return set_contract("null buffer");
+  const int k = resolve_kernel(spec, kernel);
+  if (k == FVB_KERNEL_FUSED && !fvb_fused16_supported(spec->dim, spec->p, spec->layout))
+    return set_contract("fused kernel needs p == 16");
+  if (k != FVB_KERNEL_FUSED && k != FVB_KERNEL_GENERIC) return set_contract("unknown kernel selector");
+  cudaStream_t st = as_stream(stream);
+  cudaError_t e;
+  if (zero_status) {
+    e = cudaMemsetAsync(status, 0, sizeof(uint32_t), st);
+    if (e != cudaSuccess) return set_cuda_error(e, "memset status");
+  }
+  FvbArgs a;
+  a.dim = spec->dim;
+  a.p = spec->p;
+  a.layout = spec->layout;
+  a.n = spec->n_patches;
+  a.gamma = spec->gamma;
+  a.qin = qin;
+  a.qout = qout;
+  a.cell_size = cell_size;
+  a.dt = dt;
+  a.max_eig = max_eig;
+  a.status = status;
+  if (k == FVB_KERNEL_GENERIC) {
+    // per-patch maxima are combined with atomicMax on the bit patterns
+    e = cudaMemsetAsync(max_eig, 0, sizeof(double) * (size_t)spec->n_patches, st);
+    if (e != cudaSuccess) return set_cuda_error(e, "memset max_eig");
+    e = fvb_launch_generic(a, st);
+  } else {
+    e = fvb_launch_fused16(a, st);
+  }
+  if (e != cudaSuccess) return set_cuda_error(e, "fvb_update launch");
+  return FVB_OK;
+}
+
+size_t fvb_update_host_workspace(const fvb_spec* spec, int64_t chunk) {
+  if (check_spec(spec) || chunk < 1) return 0;
+  const fvb::Geom g = fvb::make_geom(spec->dim, spec->p, chunk);
+  const size_t per = (size_t)chunk * (g.V * g.s + g.I * g.s + spec->dim + 2) * sizeof(double);
+  return 2 * per + 256;
+}
+
+int fvb_update_host(const fvb_spec* spec, const double* qin_h, double* qout_h, const double* cell_size_h,
+                    const double* dt_h, double* max_eig_h, void* workspace, size_t workspace_bytes,
+                    int64_t chunk, int kernel, void* stream) {
+  int rc = check_spec(spec);
+  if (rc) return rc;
+  if (spec->layout != 0) return set_contract("host buffers are AoS (PatchBatch layout)");
+  const int64_t n = spec->n_patches;
+  if (n == 0) return FVB_OK;
+  if (chunk < 1 || chunk > n) chunk = n;
+  if (workspace_bytes < fvb_update_host_workspace(spec, chunk)) return set_contract("workspace too small");
+  const fvb::Geom g = fvb::make_geom(spec->dim, spec->p, chunk);
+  const int d = spec->dim, s = g.s;
+  // carve the two buffer sets
+  char* base = static_cast<char*>(workspace);
+  uint32_t* status = reinterpret_cast<uint32_t*>(base);   // first 256 B: status word
+  double* bufs = reinterpret_cast<double*>(base + 256);
+  const size_t per = (size_t)chunk * (g.V * s + g.I * s + d + 2);
+  double *qin_d[2], *qout_d[2], *cs_d[2], *dt_d[2], *me_d[2];
+  for (int b = 0; b < 2; ++b) {
+    double* p = bufs + b * per;
+    qin_d[b] = p; p += (size_t)chunk * g.V * s;
+    qout_d[b] = p; p += (size_t)chunk * g.I * s;
+    cs_d[b] = p; p += (size_t)chunk * d;
+    dt_d[b] = p; p += chunk;
+    me_d[b] = p;
+  }
+  cudaStream_t comp = as_stream(stream);
+  cudaStream_t h2d = nullptr, d2h = nullptr;
+  cudaEvent_t ev_in[2] = {nullptr, nullptr}, ev_k[2] = {nullptr, nullptr}, ev_out[2] = {nullptr, nullptr};
+  cudaError_t e = cudaStreamCreateWithFlags(&h2d, cudaStreamNonBlocking);
+  if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&d2h, cudaStreamNonBlocking);
+  for (int b = 0; b < 2 && e == cudaSuccess; ++b) {
+    e = cudaEventCreateWithFlags(&ev_in[b], cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ev_k[b], cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ev_out[b], cudaEventDisableTiming);
+  }
+  if (e == cudaSuccess) e = cudaMemsetAsync(status, 0, sizeof(uint32_t), comp);
+  // the copy streams must not run ahead of the status reset / earlier work on `comp`
+  cudaEvent_t ev_start = nullptr;
+  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ev_start, cudaEventDisableTiming);
+  if (e == cudaSuccess) e = cudaEventRecord(ev_start, comp);
+  if (e == cudaSuccess) e = cudaStreamWaitEvent(h2d, ev_start, 0);
+  int nch = (int)((n + chunk - 1) / chunk);
+  int krc = FVB_OK;
+  for (int c = 0; c < nch && e == cudaSuccess && krc == FVB_OK; ++c) {
+    const int b = c & 1;
+    const int64_t p0 = (int64_t)c * chunk;
+    const int64_t np = (p0 + chunk <= n) ? chunk : n - p0;
+    if (c >= 2) e = cudaStreamWaitEvent(h2d, ev_out[b], 0);   // buffer set b drained
+    if (e == cudaSuccess)
+      e = cudaMemcpyAsync(qin_d[b], qin_h + p0 * g.V * s, (size_t)np * g.V * s * 8, cudaMemcpyHostToDevice, h2d);
+    if (e == cudaSuccess)
+      e = cudaMemcpyAsync(cs_d[b], cell_size_h + p0 * d, (size_t)np * d * 8, cudaMemcpyHostToDevice, h2d);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(dt_d[b], dt_h + p0, (size_t)np * 8, cudaMemcpyHostToDevice, h2d);
+    if (e == cudaSuccess) e = cudaEventRecord(ev_in[b], h2d);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(comp, ev_in[b], 0);
+    if (e != cudaSuccess) break;
+    fvb_spec sub = *spec;
+    sub.n_patches = np;
+    krc = fvb_update(&sub, qin_d[b], qout_d[b], cs_d[b], dt_d[b], me_d[b], status, kernel, 0, stream);
+    if (krc != FVB_OK) break;
+    e = cudaEventRecord(ev_k[b], comp);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(d2h, ev_k[b], 0);
+    if (e == cudaSuccess)
+      e = cudaMemcpyAsync(qout_h + p0 * g.I * s, qout_d[b], (size_t)np * g.I * s * 8, cudaMemcpyDeviceToHost, d2h);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(max_eig_h + p0, me_d[b], (size_t)np * 8, cudaMemcpyDeviceToHost, d2h);
+    if (e == cudaSuccess) e = cudaEventRecord(ev_out[b], d2h);
+  }
+  uint32_t st_h = 0;
+  if (e == cudaSuccess) e = cudaStreamSynchronize(d2h);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(comp);
+  if (e == cudaSuccess) e = cudaMemcpy(&st_h, status, sizeof(uint32_t), cudaMemcpyDeviceToHost);
+  for (int b = 0; b < 2; ++b) {
+    if (ev_in[b]) cudaEventDestroy(ev_in[b]);
+    if (ev_k[b]) cudaEventDestroy(ev_k[b]);
+    if (ev_out[b]) cudaEventDestroy(ev_out[b]);
+  }
+  if (ev_start) cudaEventDestroy(ev_start);
+  if (h2d) cudaStreamDestroy(h2d);
+  if (d2h) cudaStreamDestroy(d2h);
+  if (krc != FVB_OK) return krc;
+  if (e != cudaSuccess) return set_cuda_error(e, "fvb_update_host");
+  return st_h ? FVB_ERR_NONPHYSICAL : FVB_OK;
+}
+
+int fvb_locate(const fvb_spec* spec, const double* qin, fvb_boxinfo* info, void* stream) {
+  int rc = check_spec(spec);
+  if (rc) return rc;
+  if (spec->n_patches == 0) return FVB_OK;
+  static_assert(sizeof(fvb_boxinfo) == sizeof(BoxInfo), "boxinfo layout");
+  cudaError_t e = fvb_launch_locate(spec->dim, spec->p, spec->n_patches, spec->gamma, spec->layout, qin,
+                                    reinterpret_cast<BoxInfo*>(info), as_stream(stream));
+  return e == cudaSuccess ? FVB_OK : set_cuda_error(e, "fvb_locate");
+}
+
+int fvb_pack(const fvb_spec* spec, const double* aos, double* soa, int interior, void* stream) {
+  int rc = check_spec(spec);
+  if (rc) return rc;
+  const fvb::Geom g = fvb::make_geom(spec->dim, spec->p, spec->n_patches);
+  if (g.n == 0) return FVB_OK;
+  cudaError_t e = fvb_launch_pack(aos, soa, g.n, interior ? g.I : g.V, g.s, 1, as_stream(stream));
+  return e == cudaSuccess ? FVB_OK : set_cuda_error(e, "fvb_pack");
+}
+
+int fvb_unpack(const fvb_spec* spec, const double* soa, double* aos, int interior, void* stream) {
+  int rc = check_spec(spec);
+  if (rc) return rc;
+  const fvb::Geom g = fvb::make_geom(spec->dim, spec->p, spec->n_patches);
+  if (g.n == 0) return FVB_OK;
+  cudaError_t e = fvb_launch_pack(soa, aos, g.n, interior ? g.I : g.V, g.s, 0, as_stream(stream));
+  return e == cudaSuccess ? FVB_OK : set_cuda_error(e, "fvb_unpack");
+}
+
+int fvb_reduce_dt(const double* max_eig, int64_t n, double cfl, double dx, double* gmax, double* dt_scalar,
+                  double* dt_patches, int do_dt, void* stream) {
+  if (n < 1 || !max_eig || !gmax) return set_contract("reduce over an empty batch");
+  cudaError_t e = fvb_launch_reduce_dt(max_eig, n, cfl, dx, gmax, dt_scalar, dt_patches, do_dt, as_stream(stream));
+  return e == cudaSuccess ? FVB_OK : set_cuda_error(e, "fvb_reduce_dt");
+}
+
+int fvb_set_dt(const double* gmax, double cfl, double dx, double* dt_scalar, double* dt_patches, int64_t n,
+               void* stream) {
+  if (!gmax) return set_contract("null gmax");
+  cudaError_t e = fvb_launch_set_dt(gmax, cfl, dx, dt_scalar, dt_patches, n, as_stream(stream));
+  return e == cudaSuccess ? FVB_OK : set_cuda_error(e, "fvb_set_dt");
+}
+
+int fvb_patch_max_eig(const fvb_spec* spec, const double* qin, double* max_eig, uint32_t* status, void* stream) {
+  int rc = check_spec(spec);
+  if (rc) return rc;
+  if (spec->n_patches == 0) return FVB_OK;
+  cudaError_t e = fvb_launch_patch_max_eig(spec->dim, spec->p, spec->n_patches, spec->gamma, spec->layout, qin,
+                                           max_eig, status, as_stream(stream));
+  return e == cudaSuccess ? FVB_OK : set_cuda_error(e, "fvb_patch_max_eig");
+}
+
+int fvb_probe(int dim, double gamma, const double* states, int64_t n, double* lam, double* flux,
+              double* pressure, uint8_t* bad, void* stream) {
+  if (dim != 2 && dim != 3) return set_contract("dimensions must be 2 or 3");
+  if (n == 0) return FVB_OK;
+  cudaError_t e = fvb_launch_probe(dim, gamma, states, n, lam, flux, pressure, bad, as_stream(stream));
+  return e == cudaSuccess ? FVB_OK : set_cuda_error(e, "fvb_probe");
+}
+
+int fvb_selftest_div(const double* a, const double* b, double* out_shared, double* out_ieee, int64_t n,
+                     void* stream) {
+  if (n == 0) return FVB_OK;
+  cudaError_t e = fvb_launch_selftest_div(a, b, out_shared, out_ieee, n, as_stream(stream));
+  return e == cudaSuccess ? FVB_OK : set_cuda_error(e, "fvb_selftest_div");
+}
+
+}  // extern "C"

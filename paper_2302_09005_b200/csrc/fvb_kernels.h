@@ -1,0 +1,39 @@
+// fvb_kernels.h -- internal launcher interface between the C ABI and the kernels.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <cstdint>
+
+struct BoxInfo {
+  int64_t trig_rho, trig_p, first_nonpos, first_badpl;
+};
+
+struct FvbArgs {
+  int dim, p, layout;
+  int64_t n;
+  double gamma;
+  const double* qin;
+  double* qout;
+  const double* cell_size;
+  const double* dt;
+  double* max_eig;
+  unsigned* status;
+};
+
+cudaError_t fvb_launch_generic(const FvbArgs& a, cudaStream_t st);
+cudaError_t fvb_launch_fused16(const FvbArgs& a, cudaStream_t st);
+bool fvb_fused16_supported(int dim, int p, int layout);
+cudaError_t fvb_launch_locate(int dim, int p, int64_t n, double gamma, int layout, const double* qin,
+                              BoxInfo* info, cudaStream_t st);
+cudaError_t fvb_launch_pack(const double* src, double* dst, int64_t n, int64_t vols, int s, int to_soa,
+                            cudaStream_t st);
+cudaError_t fvb_launch_reduce_dt(const double* max_eig, int64_t n, double cfl, double dx, double* gmax,
+                                 double* dt_scalar, double* dt_patches, int do_dt, cudaStream_t st);
+cudaError_t fvb_launch_set_dt(const double* gmax, double cfl, double dx, double* dt_scalar, double* dt_patches,
+                              int64_t n, cudaStream_t st);
+cudaError_t fvb_launch_patch_max_eig(int dim, int p, int64_t n, double gamma, int layout, const double* qin,
+                                     double* max_eig, unsigned* status, cudaStream_t st);
+cudaError_t fvb_launch_selftest_div(const double* a, const double* b, double* out_shared, double* out_ieee,
+                                    int64_t n, cudaStream_t st);
+cudaError_t fvb_launch_probe(int dim, double gamma, const double* states, int64_t n, double* lam, double* flux,
+                             double* pressure, uint8_t* bad, cudaStream_t st);

@@ -1,0 +1,252 @@
+"""Device-side plumbing: PyTorch owns the CUDA buffers and streams, libfvb200.so computes.
+
+* `DeviceBatch`   a PatchBatch resident in HBM (AoS or packed SoA), with
+                  `update()` (fvb_update), `locate()` (fvb_locate),
+                  `max_eig_prepass()` and host round trips.
+* `update_host`   the drop-in path used by `kernel.update_patch_batch`: host
+                  numpy arrays in, host arrays out, through fvb_update_host's
+                  chunked H2D / kernel / D2H pipeline.
+* `probe`         the closure probe behind the PdeDefinition callbacks.
+
+There is no CPU fallback anywhere: without a CUDA device these raise.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import threading
+
+import numpy as np
+
+from . import _lib
+from .errors import ContractViolationError, DeviceError
+from .mesh import PatchBatch, PatchSpec
+
+LAYOUTS = {"aos": 0, "soa": 1}
+KERNELS = {"auto": _lib.KERNEL_AUTO, "generic": _lib.KERNEL_GENERIC, "fused": _lib.KERNEL_FUSED}
+
+
+def _torch():
+    import torch
+
+    if not torch.cuda.is_available():
+        raise DeviceError("no CUDA device visible: the B200 patch update has no CPU fallback")
+    return torch
+
+
+def _vp(t) -> ctypes.c_void_p:
+    return ctypes.c_void_p(t.data_ptr())
+
+
+def _hp(a: np.ndarray) -> ctypes.c_void_p:
+    return ctypes.c_void_p(a.ctypes.data)
+
+
+def _stream_handle(torch, stream) -> ctypes.c_void_p:
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return ctypes.c_void_p(s.cuda_stream)
+
+
+def kernel_id(kernel) -> int:
+    if isinstance(kernel, int):
+        return kernel
+    try:
+        return KERNELS[kernel]
+    except KeyError:
+        raise ContractViolationError(f"unknown kernel selector {kernel!r}") from None
+
+
+def selected_kernel(dim: int, p: int, n: int, gamma: float, layout: str = "aos") -> str:
+    """Name of the kernel FVB_KERNEL_AUTO resolves to for this shape."""
+    k = _lib.load().fvb_select_kernel(ctypes.byref(_lib.spec(dim, p, n, gamma, LAYOUTS[layout])))
+    return {1: "generic", 2: "fused"}.get(k, "invalid")
+
+
+class DeviceBatch:
+    """A batch of haloed patches resident in device memory.
+
+    layout "aos" keeps the reference's PatchBatch order; "soa" stores the
+    packed LayoutEnumerator(SOA) order produced by fvb_pack.
+    """
+
+    def __init__(self, spec: PatchSpec, n_patches: int, gamma: float, device=None, layout: str = "aos"):
+        torch = _torch()
+        if layout not in LAYOUTS:
+            raise ContractViolationError(f"unknown layout {layout!r}")
+        self.spec = spec
+        self.n_patches = int(n_patches)
+        self.gamma = float(gamma)
+        self.layout = layout
+        self.device = torch.device("cuda", torch.cuda.current_device() if device is None else device)
+        d, s = spec.dimensions, spec.unknowns
+        f64 = dict(dtype=torch.float64, device=self.device)
+        self.QIn = torch.empty(self.n_patches * spec.haloed_volumes * s, **f64)
+        self.QOut = torch.empty(self.n_patches * spec.interior_volumes * s, **f64)
+        self.cell_size = torch.ones(self.n_patches * d, **f64)
+        self.dt = torch.zeros(self.n_patches, **f64)
+        self.max_eigenvalue = torch.zeros(self.n_patches, **f64)
+        self.status = torch.zeros(4, dtype=torch.int32, device=self.device)
+
+    # -- construction / transfer ---------------------------------------------------------------
+    @classmethod
+    def from_host(cls, batch: PatchBatch, gamma: float, device=None, layout: str = "aos") -> "DeviceBatch":
+        torch = _torch()
+        db = cls(batch.spec, batch.n_patches, gamma, device, layout)
+        with torch.cuda.device(db.device):
+            src = torch.from_numpy(np.ascontiguousarray(batch.QIn, dtype=np.float64).reshape(-1))
+            if layout == "aos":
+                db.QIn.copy_(src)
+            else:
+                tmp = src.to(db.device)
+                db.pack_from(tmp, interior=False)
+            db.cell_size.copy_(torch.from_numpy(np.ascontiguousarray(batch.cell_size, dtype=np.float64).reshape(-1)))
+            db.dt.copy_(torch.from_numpy(np.ascontiguousarray(batch.dt, dtype=np.float64)))
+        return db
+
+    def fvb_spec(self) -> _lib.FvbSpec:
+        return _lib.spec(self.spec.dimensions, self.spec.volumes_per_axis, self.n_patches, self.gamma,
+                         LAYOUTS[self.layout])
+
+    def pack_from(self, aos_qin, interior: bool = False, stream=None):
+        """Fill QIn (or QOut if interior) from an AoS device tensor via fvb_pack."""
+        torch = _torch()
+        dst = self.QOut if interior else self.QIn
+        _lib.check(_lib.load().fvb_pack(ctypes.byref(self.fvb_spec()), _vp(aos_qin), _vp(dst), int(interior),
+                                        _stream_handle(torch, stream)), "fvb_pack")
+
+    def qout_aos(self, stream=None):
+        """QOut in the reference's AoS order (unpacked on the device for SoA batches)."""
+        torch = _torch()
+        if self.layout == "aos":
+            return self.QOut
+        out = torch.empty_like(self.QOut)
+        _lib.check(_lib.load().fvb_unpack(ctypes.byref(self.fvb_spec()), _vp(self.QOut), _vp(out), 1,
+                                          _stream_handle(torch, stream)), "fvb_unpack")
+        return out
+
+    # -- compute --------------------------------------------------------------------------------
+    def update(self, kernel="auto", stream=None, zero_status: bool = True) -> None:
+        """One Rusanov step, asynchronous on `stream` (torch's current stream by default)."""
+        torch = _torch()
+        _lib.check(_lib.load().fvb_update(
+            ctypes.byref(self.fvb_spec()), _vp(self.QIn), _vp(self.QOut), _vp(self.cell_size), _vp(self.dt),
+            _vp(self.max_eigenvalue), _vp(self.status), kernel_id(kernel), int(zero_status),
+            _stream_handle(torch, stream)), "fvb_update")
+
+    def max_eig_prepass(self, stream=None) -> None:
+        """Per-patch wave speed of QIn without an update (first-step dt)."""
+        torch = _torch()
+        self.max_eigenvalue.zero_()
+        _lib.check(_lib.load().fvb_patch_max_eig(ctypes.byref(self.fvb_spec()), _vp(self.QIn),
+                                                 _vp(self.max_eigenvalue), _vp(self.status),
+                                                 _stream_handle(torch, stream)), "fvb_patch_max_eig")
+
+    def nonphysical(self) -> bool:
+        return bool(int(self.status[0].item()) != 0)
+
+    def locate(self, stream=None) -> np.ndarray:
+        """Per-(patch, box) diagnostics (n, 2d+1, 4) int64 -- the error path."""
+        torch = _torch()
+        nbox = 2 * self.spec.dimensions + 1
+        info = torch.empty(self.n_patches * nbox * 4, dtype=torch.int64, device=self.device)
+        _lib.check(_lib.load().fvb_locate(ctypes.byref(self.fvb_spec()), _vp(self.QIn), _vp(info),
+                                          _stream_handle(torch, stream)), "fvb_locate")
+        return info.cpu().numpy().reshape(self.n_patches, nbox, 4)
+
+    def to_host(self, batch: PatchBatch) -> None:
+        """Copy QOut (AoS) and max_eigenvalue back into a host PatchBatch."""
+        batch.QOut.reshape(-1)[...] = self.qout_aos().cpu().numpy()
+        batch.max_eigenvalue[...] = self.max_eigenvalue.cpu().numpy()
+
+
+# --- host-buffer path -----------------------------------------------------------------------------
+
+_tls = threading.local()
+
+
+def _workspace(torch, device, nbytes: int):
+    """Per-thread, per-device workspace and stream (concurrent calls on disjoint batches are legal)."""
+    cache = getattr(_tls, "cache", None)
+    if cache is None:
+        cache = _tls.cache = {}
+    key = device.index
+    ws, stream = cache.get(key, (None, None))
+    if ws is None or ws.numel() < nbytes:
+        ws = torch.empty(nbytes, dtype=torch.uint8, device=device)
+    if stream is None:
+        stream = torch.cuda.Stream(device=device)
+    cache[key] = (ws, stream)
+    return ws, stream
+
+
+def default_chunk(spec: PatchSpec, n: int) -> int:
+    per_patch = (spec.haloed_volumes + spec.interior_volumes) * spec.unknowns * 8
+    by_bytes = max(1, (256 << 20) // per_patch)
+    by_pipeline = max(1, -(-n // 8))
+    return int(max(1, min(n, by_bytes, max(by_pipeline, min(n, 64)))))
+
+
+def update_host(batch: PatchBatch, gamma: float, device=None, kernel="auto", chunk_patches: int | None = None):
+    """fvb_update_host on the batch's numpy arrays.  Returns the C-ABI code (0 or FVB_ERR_NONPHYSICAL)."""
+    torch = _torch()
+    dev = torch.device("cuda", torch.cuda.current_device() if device is None else device)
+    spec = batch.spec
+    n = batch.n_patches
+    chunk = int(chunk_patches or default_chunk(spec, n))
+    fs = _lib.spec(spec.dimensions, spec.volumes_per_axis, n, gamma, 0)
+    L = _lib.load()
+    need = L.fvb_update_host_workspace(ctypes.byref(fs), chunk)
+    arrays = []
+    for name in ("QIn", "QOut", "cell_size", "dt", "max_eigenvalue"):
+        a = getattr(batch, name)
+        if a.dtype != np.float64 or not a.flags.c_contiguous:
+            raise ContractViolationError(f"batch.{name} must be a C-contiguous float64 array")
+        arrays.append(a)
+    with torch.cuda.device(dev):
+        ws, stream = _workspace(torch, dev, need)
+        rc = L.fvb_update_host(ctypes.byref(fs), _hp(batch.QIn), _hp(batch.QOut), _hp(batch.cell_size),
+                               _hp(batch.dt), _hp(batch.max_eigenvalue), _vp(ws), ctypes.c_size_t(ws.numel()),
+                               chunk, kernel_id(kernel), ctypes.c_void_p(stream.cuda_stream))
+    if rc not in (_lib.FVB_OK, _lib.FVB_ERR_NONPHYSICAL):
+        _lib.check(rc, "fvb_update_host")
+    return rc
+
+
+def locate_host(batch: PatchBatch, gamma: float, device=None, chunk_patches: int | None = None) -> np.ndarray:
+    """fvb_locate over a host batch, chunk by chunk (error path only)."""
+    torch = _torch()
+    dev = torch.device("cuda", torch.cuda.current_device() if device is None else device)
+    spec = batch.spec
+    n = batch.n_patches
+    d = spec.dimensions
+    nbox = 2 * d + 1
+    chunk = int(chunk_patches or default_chunk(spec, n))
+    out = np.empty((n, nbox, 4), dtype=np.int64)
+    L = _lib.load()
+    with torch.cuda.device(dev):
+        for p0 in range(0, n, chunk):
+            p1 = min(n, p0 + chunk)
+            q = torch.from_numpy(np.ascontiguousarray(batch.QIn[p0:p1]).reshape(-1)).to(dev)
+            info = torch.empty((p1 - p0) * nbox * 4, dtype=torch.int64, device=dev)
+            fs = _lib.spec(d, spec.volumes_per_axis, p1 - p0, gamma, 0)
+            _lib.check(L.fvb_locate(ctypes.byref(fs), _vp(q), _vp(info),
+                                    _stream_handle(torch, None)), "fvb_locate")
+            out[p0:p1] = info.cpu().numpy().reshape(p1 - p0, nbox, 4)
+    return out
+
+
+def probe(dim: int, gamma: float, states: np.ndarray):
+    """(lam (n,d), flux (n,d,s), pressure (n,), bad (n,)) of AoS states, on the device."""
+    torch = _torch()
+    n = states.shape[0]
+    s = dim + 2
+    dev = torch.device("cuda", torch.cuda.current_device())
+    q = torch.from_numpy(np.ascontiguousarray(states, dtype=np.float64).reshape(-1)).to(dev)
+    lam = torch.empty(n * dim, dtype=torch.float64, device=dev)
+    flux = torch.empty(n * dim * s, dtype=torch.float64, device=dev)
+    pres = torch.empty(max(n, 1), dtype=torch.float64, device=dev)
+    bad = torch.zeros(max(n, 1), dtype=torch.uint8, device=dev)
+    _lib.check(_lib.load().fvb_probe(dim, gamma, _vp(q), n, _vp(lam), _vp(flux), _vp(pres), _vp(bad),
+                                     _stream_handle(torch, None)), "fvb_probe")
+    return (lam.cpu().numpy().reshape(n, dim), flux.cpu().numpy().reshape(n, dim, s),
+            pres.cpu().numpy()[:n], bad.cpu().numpy()[:n])

@@ -1,0 +1,80 @@
+"""Multi-step / multi-GPU driver: the CFL step around the fused patch update.
+
+SPEC.md:446-449 (run_simulation, no code in the reference) fixes the global
+time step as dt = cflFactor * dx / max_patches maxEigenvalue, using the
+previous step's per-patch maxima (a wave-speed pre-pass for the first step,
+SPEC.md:467).  One process drives one GPU (torch.distributed, NCCL over
+NVLink); patches are sharded contiguously across ranks, and the only
+exchange of the step is one 8-byte MAX all-reduce of the wave speed.
+
+Per step, entirely on the device and asynchronous on one stream:
+
+    fvb_update            fused Rusanov update of the local shard
+    fvb_reduce_dt(do_dt=0) local max of max_eigenvalue -> gmax (1 double)
+    all_reduce(gmax, MAX)  NCCL, only when world_size > 1
+    fvb_set_dt             dt = (cfl*dx)/gmax broadcast into the shard's dt[]
+"""
+
+from __future__ import annotations
+
+import ctypes
+
+from . import _lib
+from .device import DeviceBatch, _stream_handle, _torch, _vp
+
+
+def shard_bounds(n: int, rank: int, world: int) -> tuple[int, int]:
+    """Contiguous patch range of a rank (preserves the global patch order)."""
+    base, extra = divmod(n, world)
+    lo = rank * base + min(rank, extra)
+    return lo, lo + base + (1 if rank < extra else 0)
+
+
+class CflStepper:
+    """Device-resident step loop for one shard."""
+
+    def __init__(self, db: DeviceBatch, cfl: float = 0.4, dx: float | None = None, group=None,
+                 kernel="auto", stream=None):
+        torch = _torch()
+        self.db = db
+        self.cfl = float(cfl)
+        self.dx = float(dx) if dx is not None else float(db.cell_size[0].item()) / db.spec.volumes_per_axis
+        self.group = group
+        self.kernel = kernel
+        self.stream = stream
+        self.gmax = torch.zeros(1, dtype=torch.float64, device=db.device)
+        self.dt_scalar = torch.zeros(1, dtype=torch.float64, device=db.device)
+        import torch.distributed as dist
+
+        self._dist = dist if (dist.is_available() and dist.is_initialized()) else None
+
+    def reduce_dt(self) -> None:
+        torch = _torch()
+        L = _lib.load()
+        st = _stream_handle(torch, self.stream)
+        if self._dist is None or self._dist.get_world_size(self.group) == 1:
+            _lib.check(L.fvb_reduce_dt(_vp(self.db.max_eigenvalue), self.db.n_patches, self.cfl, self.dx,
+                                       _vp(self.gmax), _vp(self.dt_scalar), _vp(self.db.dt), 1, st), "fvb_reduce_dt")
+            return
+        _lib.check(L.fvb_reduce_dt(_vp(self.db.max_eigenvalue), self.db.n_patches, self.cfl, self.dx,
+                                   _vp(self.gmax), None, None, 0, st), "fvb_reduce_dt")
+        self._dist.all_reduce(self.gmax, op=self._dist.ReduceOp.MAX, group=self.group)
+        _lib.check(L.fvb_set_dt(_vp(self.gmax), self.cfl, self.dx, _vp(self.dt_scalar), _vp(self.db.dt),
+                                self.db.n_patches, st), "fvb_set_dt")
+
+    def prepass(self) -> None:
+        """First-step dt from the initial wave speeds."""
+        self.db.max_eig_prepass(stream=self.stream)
+        self.reduce_dt()
+
+    def step(self) -> None:
+        """update -> local max -> (all-reduce) -> dt, all enqueued on the stream."""
+        self.db.update(kernel=self.kernel, stream=self.stream)
+        self.reduce_dt()
+
+
+def cfl_dt(db: DeviceBatch, cfl: float = 0.4, dx: float | None = None, group=None):
+    """(global max wave speed, dt) from db.max_eigenvalue; synchronises."""
+    s = CflStepper(db, cfl, dx, group)
+    s.reduce_dt()
+    return float(s.gmax.item()), float(s.dt_scalar.item())
