@@ -26,6 +26,8 @@
 // exactly the reference's and needs no sign-of-zero special cases.
 #include <cuda_runtime.h>
 
+#include <cstdlib>
+
 #include "fvb_exact.cuh"
 #include "fvb_kernels.h"
 #include "fvb_layout.cuh"
@@ -174,8 +176,8 @@ __device__ __forceinline__ void flux_term(double (&F)[D + 2], double inv, double
   }
 }
 
-template <int D, int L>
-__global__ void __launch_bounds__(288, 2)
+template <int D, int L, int MINB>
+__global__ void __launch_bounds__(288, MINB)
 fused16_kernel(const double* __restrict__ qin, double* __restrict__ qout, const double* __restrict__ cell_size,
                const double* __restrict__ dtv, double* __restrict__ max_eig, unsigned* __restrict__ status,
                int64_t n, Closure cl) {
@@ -414,6 +416,9 @@ fused16_kernel(const double* __restrict__ qin, double* __restrict__ qout, const 
         cm = 0;
       }
     }
+    // 3D: phase A of the next plane overwrites the y/x-side buffers (parity of
+    // plane zh-1) that phase B just read, so every warp must be past phase B.
+    if (D == 3) __syncthreads();
   }
 
   const int any_bad = __syncthreads_or(bad ? 1 : 0);
@@ -425,24 +430,38 @@ fused16_kernel(const double* __restrict__ qin, double* __restrict__ qout, const 
   if (tid == 0 && any_bad) atomicOr(status, 1u);
 }
 
-template <int D, int L>
-cudaError_t launch(const FvbArgs& a, cudaStream_t st) {
+// FVB_FUSED_MINB=1 selects the 1-CTA/SM build (no register cap); default 2 CTAs/SM.
+static int min_blocks_choice() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("FVB_FUSED_MINB");
+    v = (e && e[0] == '1') ? 1 : 2;
+  }
+  return v;
+}
+
+template <int D, int L, int MINB>
+cudaError_t launch_impl(const FvbArgs& a, cudaStream_t st) {
   using C = Cfg<D, L>;
-  cudaError_t e = cudaFuncSetAttribute(fused16_kernel<D, L>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)C::BYTES);
+  auto kfn = fused16_kernel<D, L, MINB>;
+  cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::BYTES);
   if (e != cudaSuccess) return e;
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   int per_sm = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fused16_kernel<D, L>, 288, C::BYTES);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kfn, 288, C::BYTES);
   if (per_sm < 1) per_sm = 1;
   int64_t grid = (int64_t)sms * per_sm;
   if (grid > a.n) grid = a.n;
   const Closure cl{a.gamma, a.gamma - 1.0};
-  fused16_kernel<D, L><<<(unsigned)grid, 288, C::BYTES, st>>>(a.qin, a.qout, a.cell_size, a.dt, a.max_eig,
-                                                                a.status, a.n, cl);
+  kfn<<<(unsigned)grid, 288, C::BYTES, st>>>(a.qin, a.qout, a.cell_size, a.dt, a.max_eig, a.status, a.n, cl);
   return cudaGetLastError();
+}
+
+template <int D, int L>
+cudaError_t launch(const FvbArgs& a, cudaStream_t st) {
+  return min_blocks_choice() == 1 ? launch_impl<D, L, 1>(a, st) : launch_impl<D, L, 2>(a, st);
 }
 
 }  // namespace f16
