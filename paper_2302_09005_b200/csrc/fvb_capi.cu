@@ -82,7 +82,7 @@ int fvb_update(const fvb_spec* spec, const double* qin, double* qout, const doub
   cudaStream_t st = as_stream(stream);
   cudaError_t e;
   if (zero_status) {
-    e = cudaMemsetAsync(status, 0, sizeof(uint32_t), st);
+    e = cudaMemsetAsync(status, 0, 2 * sizeof(uint32_t), st);   // flag + redo count
     if (e != cudaSuccess) return set_cuda_error(e, "memset status");
   }
   FvbArgs a;
@@ -109,11 +109,15 @@ int fvb_update(const fvb_spec* spec, const double* qin, double* qout, const doub
   return FVB_OK;
 }
 
+static size_t status_bytes(int64_t chunk) { return ((size_t)(chunk + 2) * 4 + 255) / 256 * 256; }
+
+size_t fvb_status_words(int64_t n_patches) { return (size_t)(n_patches + 2); }
+
 size_t fvb_update_host_workspace(const fvb_spec* spec, int64_t chunk) {
   if (check_spec(spec) || chunk < 1) return 0;
   const fvb::Geom g = fvb::make_geom(spec->dim, spec->p, chunk);
   const size_t per = (size_t)chunk * (g.V * g.s + g.I * g.s + spec->dim + 2) * sizeof(double);
-  return 2 * per + 256;
+  return 2 * per + 2 * status_bytes(chunk);
 }
 
 int fvb_update_host(const fvb_spec* spec, const double* qin_h, double* qout_h, const double* cell_size_h,
@@ -130,8 +134,10 @@ int fvb_update_host(const fvb_spec* spec, const double* qin_h, double* qout_h, c
   const int d = spec->dim, s = g.s;
   // carve the two buffer sets
   char* base = static_cast<char*>(workspace);
-  uint32_t* status = reinterpret_cast<uint32_t*>(base);   // first 256 B: status word
-  double* bufs = reinterpret_cast<double*>(base + 256);
+  // two status buffers (flag, redo count, redo list), one per buffer set
+  uint32_t* status_b[2] = {reinterpret_cast<uint32_t*>(base),
+                           reinterpret_cast<uint32_t*>(base + status_bytes(chunk))};
+  double* bufs = reinterpret_cast<double*>(base + 2 * status_bytes(chunk));
   const size_t per = (size_t)chunk * (g.V * s + g.I * s + d + 2);
   double *qin_d[2], *qout_d[2], *cs_d[2], *dt_d[2], *me_d[2];
   for (int b = 0; b < 2; ++b) {
@@ -152,7 +158,9 @@ int fvb_update_host(const fvb_spec* spec, const double* qin_h, double* qout_h, c
     if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ev_k[b], cudaEventDisableTiming);
     if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ev_out[b], cudaEventDisableTiming);
   }
-  if (e == cudaSuccess) e = cudaMemsetAsync(status, 0, sizeof(uint32_t), comp);
+  // flag words of both status buffers accumulate over the chunks; redo counts are reset per chunk
+  if (e == cudaSuccess) e = cudaMemsetAsync(status_b[0], 0, 8, comp);
+  if (e == cudaSuccess) e = cudaMemsetAsync(status_b[1], 0, 8, comp);
   // the copy streams must not run ahead of the status reset / earlier work on `comp`
   cudaEvent_t ev_start = nullptr;
   if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ev_start, cudaEventDisableTiming);
@@ -175,7 +183,9 @@ int fvb_update_host(const fvb_spec* spec, const double* qin_h, double* qout_h, c
     if (e != cudaSuccess) break;
     fvb_spec sub = *spec;
     sub.n_patches = np;
-    krc = fvb_update(&sub, qin_d[b], qout_d[b], cs_d[b], dt_d[b], me_d[b], status, kernel, 0, stream);
+    e = cudaMemsetAsync(status_b[b] + 1, 0, 4, comp);   // redo count of this chunk
+    if (e != cudaSuccess) break;
+    krc = fvb_update(&sub, qin_d[b], qout_d[b], cs_d[b], dt_d[b], me_d[b], status_b[b], kernel, 0, stream);
     if (krc != FVB_OK) break;
     e = cudaEventRecord(ev_k[b], comp);
     if (e == cudaSuccess) e = cudaStreamWaitEvent(d2h, ev_k[b], 0);
@@ -184,10 +194,11 @@ int fvb_update_host(const fvb_spec* spec, const double* qin_h, double* qout_h, c
     if (e == cudaSuccess) e = cudaMemcpyAsync(max_eig_h + p0, me_d[b], (size_t)np * 8, cudaMemcpyDeviceToHost, d2h);
     if (e == cudaSuccess) e = cudaEventRecord(ev_out[b], d2h);
   }
-  uint32_t st_h = 0;
+  uint32_t st_h[2] = {0, 0};
   if (e == cudaSuccess) e = cudaStreamSynchronize(d2h);
   if (e == cudaSuccess) e = cudaStreamSynchronize(comp);
-  if (e == cudaSuccess) e = cudaMemcpy(&st_h, status, sizeof(uint32_t), cudaMemcpyDeviceToHost);
+  if (e == cudaSuccess) e = cudaMemcpy(&st_h[0], status_b[0], sizeof(uint32_t), cudaMemcpyDeviceToHost);
+  if (e == cudaSuccess) e = cudaMemcpy(&st_h[1], status_b[1], sizeof(uint32_t), cudaMemcpyDeviceToHost);
   for (int b = 0; b < 2; ++b) {
     if (ev_in[b]) cudaEventDestroy(ev_in[b]);
     if (ev_k[b]) cudaEventDestroy(ev_k[b]);
@@ -198,7 +209,7 @@ int fvb_update_host(const fvb_spec* spec, const double* qin_h, double* qout_h, c
   if (d2h) cudaStreamDestroy(d2h);
   if (krc != FVB_OK) return krc;
   if (e != cudaSuccess) return set_cuda_error(e, "fvb_update_host");
-  return st_h ? FVB_ERR_NONPHYSICAL : FVB_OK;
+  return (st_h[0] | st_h[1]) ? FVB_ERR_NONPHYSICAL : FVB_OK;
 }
 
 int fvb_locate(const fvb_spec* spec, const double* qin, fvb_boxinfo* info, void* stream) {

@@ -1,0 +1,408 @@
+// fvb_fused3d.cu -- fused 3D Rusanov patch update for p = 16 (the headline shape).
+//
+// One persistent CTA (8 "interior" warps + 1 "halo" warp, 2 CTAs per SM)
+// marches each patch plane by plane in z:
+//
+//   ring    4 TMA bulk-copy stages of one haloed z-plane (18x18x5 doubles,
+//           12,960 B), mbarrier complete_tx; plane g+2 is issued while plane g
+//           is consumed.
+//   xs, ys  x- and y-side data (lam, f[1..4]) of every volume of the plane,
+//           including the face-halo columns / rows (written by the halo
+//           warp), double-buffered by plane parity.
+//   ostage  one output plane (16x16x5) stored back with a TMA bulk store.
+//
+// Iteration g (haloed plane zh):
+//   A  interior lanes evaluate the Euler closure of their volume of plane zh
+//      once (14 quotients sharing one reciprocal refinement, fvb_exact.cuh)
+//      and publish its x/y-side data; the halo warp publishes the x/y face
+//      halo volumes.                                             -- barrier
+//   B  interior lanes update their cell of plane zh-1 from the published
+//      side data (x and y faces evaluated from both sides, exactly as the
+//      reference's per-volume passes), and the z faces marching in
+//      registers: the face (zh-1 | zh) is evaluated once and re-used, negated,
+//      as the minus face of the next plane.                      -- barrier
+//
+// The re-used z face is the only place the arithmetic is not literally the
+// reference's: -RN(c*(a-b)) equals RN(c*(b-a)) except for the sign of an
+// exact zero, which can only surface as a -0.0 result where the reference
+// has +0.0; the epilogue fixes exactly that case (see fix_negzero).
+#include <cuda_runtime.h>
+
+#include <cstdlib>
+
+#include "fvb_exact.cuh"
+#include "fvb_kernels.h"
+#include "fvb_layout.cuh"
+#include "fvb_tma.cuh"
+
+namespace fvb {
+namespace f3 {
+
+using namespace f16;
+
+constexpr int P = 16, E = 18, S = 5;
+constexpr int PLANE = E * E;              // haloed volumes per plane
+constexpr int STAGE = PLANE * S;          // doubles per ring stage
+constexpr int NST = 4;
+constexpr int NPL = E;                    // planes per patch
+constexpr int64_t VOL = (int64_t)E * E * E;
+constexpr int64_t IVOL = (int64_t)P * P * P;
+constexpr int SIDE = S * E * P;           // one x- or y-side buffer: 5 comps x 18 x 16
+constexpr int OUTN = P * P * S;
+constexpr int OFF_RING = 0;
+constexpr int OFF_YS = OFF_RING + NST * STAGE;
+constexpr int OFF_XS = OFF_YS + 2 * SIDE;
+constexpr int OFF_OUT = OFF_XS + 2 * SIDE;
+constexpr int OFF_WMAX = OFF_OUT + OUTN;
+constexpr int OFF_FLAG = OFF_WMAX + 16;
+constexpr int OFF_BAR = OFF_FLAG + 1;
+constexpr int TOTAL = OFF_BAR + NST;
+constexpr size_t BYTES = (size_t)TOTAL * 8;
+
+template <int L>
+__device__ __forceinline__ double qs(const double* st, int hy, int hx, int u) {
+  return L == kAoS ? st[(hy * E + hx) * S + u] : st[(u * E + hy) * E + hx];
+}
+template <int L>
+__device__ __forceinline__ void load_q(const double* st, int hy, int hx, double (&q)[S]) {
+#pragma unroll
+  for (int u = 0; u < S; ++u) q[u] = qs<L>(st, hy, hx, u);
+}
+// ys: [c][haloed row hy][interior col x];  xs: [c][interior row y][haloed col hx]
+__device__ __forceinline__ int ys_at(int c, int hy, int x) { return (c * E + hy) * P + x; }
+__device__ __forceinline__ int xs_at(int c, int y, int hx) { return (c * P + y) * E + hx; }
+
+__device__ __forceinline__ void put_ys(double* b, int hy, int x, const Side<3>& s) {
+  b[ys_at(0, hy, x)] = s.lam;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) b[ys_at(k + 1, hy, x)] = s.f[k];
+}
+__device__ __forceinline__ void put_xs(double* b, int y, int hx, const Side<3>& s) {
+  b[xs_at(0, y, hx)] = s.lam;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) b[xs_at(k + 1, y, hx)] = s.f[k];
+}
+
+// vectorized.py:193-200 for one direction: inv*(0.5*(f_m+f_c) - 0.5*(f_c+f_p)),
+// component u of the three fluxes supplied by `fm/fc/fp(u)`.
+template <class FM, class FC, class FP>
+__device__ __forceinline__ void add_flux(double (&val)[S], double inv, FM fm, FC fc, FP fp) {
+#pragma unroll
+  for (int u = 0; u < S; ++u) {
+    const double c = fc(u);
+    const double favg_m = dmul(0.5, dadd(fm(u), c));
+    const double favg_p = dmul(0.5, dadd(c, fp(u)));
+    val[u] = dadd(val[u], dmul(inv, dsub(favg_m, favg_p)));
+  }
+}
+
+__device__ __forceinline__ bool is_negzero(double v) {
+  return (unsigned long long)__double_as_longlong(v) == 0x8000000000000000ull;
+}
+
+template <int L, int MINB>
+__global__ void __launch_bounds__(288, MINB)
+fused3d_kernel(const double* __restrict__ qin, double* __restrict__ qout, const double* __restrict__ cell_size,
+               const double* __restrict__ dtv, double* __restrict__ max_eig, unsigned* __restrict__ status,
+               int64_t n, Closure cl) {
+  extern __shared__ __align__(128) double sm[];
+  double* ring = sm + OFF_RING;
+  double* ysb = sm + OFF_YS;
+  double* xsb = sm + OFF_XS;
+  double* outb = sm + OFF_OUT;
+  unsigned long long* wmax = reinterpret_cast<unsigned long long*>(sm + OFF_WMAX);
+  unsigned* slowflag = reinterpret_cast<unsigned*>(sm + OFF_FLAG);   // 2 words, by patch parity
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sm + OFF_BAR);
+
+  const int tid = threadIdx.x;
+  const bool interior = tid < 256;
+  const int warp = tid >> 5, lane = tid & 31;
+  const int x = lane & 15;
+  const int y = ((warp & 7) << 1) | (lane >> 4);
+  const bool producer = tid == 256;
+
+  const int64_t my_patches = (n > (int64_t)blockIdx.x) ? (n - 1 - (int64_t)blockIdx.x) / gridDim.x + 1 : 0;
+  const int64_t G = my_patches * NPL;
+  auto patch_of = [&](int64_t g) -> int64_t { return (int64_t)blockIdx.x + (g / NPL) * (int64_t)gridDim.x; };
+
+  auto issue = [&](int64_t g) {
+    const int64_t pidx = patch_of(g);
+    const int zh = (int)(g % NPL);
+    double* st = ring + (g % NST) * STAGE;
+    uint64_t* bar = bars + (g % NST);
+    fence_proxy_async();
+    mbar_expect_tx(bar, (uint32_t)(STAGE * 8));
+    if (L == kAoS) {
+      tma_load_1d(st, qin + (pidx * VOL + (int64_t)zh * PLANE) * S, (uint32_t)(STAGE * 8), bar);
+    } else {
+#pragma unroll
+      for (int u = 0; u < S; ++u)
+        tma_load_1d(st + u * PLANE, qin + ((int64_t)u * n + pidx) * VOL + (int64_t)zh * PLANE,
+                    (uint32_t)(PLANE * 8), bar);
+    }
+  };
+  auto store_out = [&](int64_t g) {   // output of iteration g: interior plane zh-2
+    const int64_t pidx = patch_of(g);
+    const int z = (int)(g % NPL) - 2;
+    if (L == kAoS) {
+      tma_store_1d(qout + (pidx * IVOL + (int64_t)z * P * P) * S, outb, (uint32_t)(OUTN * 8));
+    } else {
+#pragma unroll
+      for (int u = 0; u < S; ++u)
+        tma_store_1d(qout + ((int64_t)u * n + pidx) * IVOL + (int64_t)z * P * P, outb + u * P * P,
+                     (uint32_t)(P * P * 8));
+    }
+    bulk_commit();
+  };
+  auto finish_patch_max = [&](int64_t j) {
+    unsigned long long m = wmax[(j & 1) * 8];
+#pragma unroll
+    for (int w = 1; w < 8; ++w) {
+      const unsigned long long v = wmax[(j & 1) * 8 + w];
+      m = v > m ? v : m;
+    }
+    const int64_t pidx = (int64_t)blockIdx.x + j * (int64_t)gridDim.x;
+    max_eig[pidx] = __longlong_as_double((long long)m);
+    if (slowflag[j & 1]) {   // queue the patch for the exact re-evaluation (fvb_redo_kernel)
+      const unsigned k = atomicAdd(&status[1], 1u);
+      status[2 + k] = (unsigned)pidx;
+      slowflag[j & 1] = 0;
+    }
+  };
+
+  if (producer) {
+#pragma unroll
+    for (int s = 0; s < NST; ++s) mbar_init(&bars[s], 1);
+    slowflag[0] = slowflag[1] = 0;
+    fence_mbar_init();
+  }
+  __syncthreads();
+  if (producer)
+    for (int64_t g = 0; g < 2 && g < G; ++g) issue(g);
+
+  bool bad = false;
+  unsigned long long cm = 0;   // running max wave speed (bit pattern) of this column
+  double inv = 0.0, half_inv = 0.0;
+  // z-march carries: z-side data of the previous plane, and the previous z face
+  // (its dissipation term seen from the lower cell, tp, and its flux average)
+  Side<3> zprev;
+  double tp[S], favg_zm[S];
+  zprev.lam = 0.0;
+#pragma unroll
+  for (int u = 0; u < S; ++u) { tp[u] = 0.0; favg_zm[u] = 0.0; }
+#pragma unroll
+  for (int k = 0; k < 4; ++k) zprev.f[k] = 0.0;
+
+  for (int64_t g = 0; g < G; ++g) {
+    const int zh = (int)(g % NPL);
+    const int64_t pidx = patch_of(g);
+    if (zh == 0) {
+      const double dx = __ddiv_rn(cell_size[pidx * 3], (double)P);   // vectorized.py:169
+      inv = __ddiv_rn(dtv[pidx], dx);                                  // vectorized.py:170
+      half_inv = dmul(0.5, inv);                                       // `0.5 * inv * a`
+    }
+    const double* st = ring + (g % NST) * STAGE;
+    mbar_wait(&bars[g % NST], (uint32_t)((g / NST) & 1));
+    const bool full_plane = zh >= 1 && zh <= P;
+    double* ys_w = ysb + (g & 1) * SIDE;
+    double* xs_w = xsb + (g & 1) * SIDE;
+
+    // ---------------- A: closures of plane zh ----------------
+    Side<3> zcur;
+    if (interior) {
+      double q[S];
+      load_q<L>(st, y + 1, x + 1, q);
+      if (full_plane) {
+        Side<3> sd[3];
+        bool ok;
+        const Thermo<3> T = closure_all_fast<3>(q, cl, sd, ok);
+        bad = bad || (ok && T.bad);
+        if (!ok) atomicOr(&slowflag[(g / NPL) & 1], 1u);
+        unsigned long long m = (unsigned long long)__double_as_longlong(sd[0].lam);
+        unsigned long long v = (unsigned long long)__double_as_longlong(sd[1].lam);
+        m = v > m ? v : m;
+        v = (unsigned long long)__double_as_longlong(sd[2].lam);
+        m = v > m ? v : m;
+        cm = m > cm ? m : cm;
+        put_xs(xs_w, y, x + 1, sd[0]);
+        put_ys(ys_w, y + 1, x, sd[1]);
+        zcur = sd[2];
+      } else {
+        bool ok;
+        const Thermo<3> T = closure_one_fast<3>(q, cl, 2, zcur, ok);
+        bad = bad || (ok && T.bad);
+        if (!ok) atomicOr(&slowflag[(g / NPL) & 1], 1u);
+      }
+    } else if (full_plane) {
+      {   // y-face halo rows (haloed y = 0, 17), interior columns
+        const int hy = lane < 16 ? 0 : E - 1;
+        double q[S];
+        load_q<L>(st, hy, x + 1, q);
+        Side<3> sh;
+        bool ok;
+        const Thermo<3> T = closure_one_fast<3>(q, cl, 1, sh, ok);
+        bad = bad || (ok && T.bad);
+        if (!ok) atomicOr(&slowflag[(g / NPL) & 1], 1u);
+        put_ys(ys_w, hy, x, sh);
+      }
+      {   // x-face halo columns (haloed x = 0, 17), interior rows
+        const int hx = lane < 16 ? 0 : E - 1;
+        double q[S];
+        load_q<L>(st, x + 1, hx, q);
+        Side<3> sh;
+        bool ok;
+        const Thermo<3> T = closure_one_fast<3>(q, cl, 0, sh, ok);
+        bad = bad || (ok && T.bad);
+        if (!ok) atomicOr(&slowflag[(g / NPL) & 1], 1u);
+        put_xs(xs_w, x, hx, sh);
+      }
+    }
+    if (producer) bulk_wait_read0();   // ostage read by its TMA store
+    __syncthreads();
+    if (producer) {
+      if (g + 2 < G) issue(g + 2);    // into the stage of plane g-2, unused from here on
+      if (g >= 1 && (g - 1) % NPL == NPL - 1) finish_patch_max((g - 1) / NPL);
+    }
+
+    // ---------------- B: update of the cells of plane zh-1 ----------------
+    if (interior && zh >= 1) {
+      const double* stc = ring + ((g + NST - 1) % NST) * STAGE;   // plane zh-1
+      const double* ys_r = ysb + ((g - 1) & 1) * SIDE;
+      const double* xs_r = xsb + ((g - 1) & 1) * SIDE;
+      double qc[S], val[S], qn[S];
+      load_q<L>(stc, y + 1, x + 1, qc);
+      // z face (zh-1 | zh) seen from the lower cell: coeff*(Q_zh - Q_zh-1)
+      const double cz = dmul(half_inv, speed_max(zcur.lam, zprev.lam));
+      if (zh >= 2) {
+#pragma unroll
+        for (int u = 0; u < S; ++u) val[u] = qc[u];                       // _pass_copy
+        // dissipation x-, x+, y-, y+ (vectorized.py:173-180)
+        const double lx = xs_r[xs_at(0, y, x + 1)];
+        load_q<L>(stc, y + 1, x, qn);
+        dissipate<3>(val, half_inv, lx, qc, xs_r[xs_at(0, y, x)], qn);
+        load_q<L>(stc, y + 1, x + 2, qn);
+        dissipate<3>(val, half_inv, lx, qc, xs_r[xs_at(0, y, x + 2)], qn);
+        const double ly = ys_r[ys_at(0, y + 1, x)];
+        load_q<L>(stc, y, x + 1, qn);
+        dissipate<3>(val, half_inv, ly, qc, ys_r[ys_at(0, y, x)], qn);
+        load_q<L>(stc, y + 2, x + 1, qn);
+        dissipate<3>(val, half_inv, ly, qc, ys_r[ys_at(0, y + 2, x)], qn);
+        // z-: the previous face's term, negated; z+: this face's term
+#pragma unroll
+        for (int u = 0; u < S; ++u) val[u] = dsub(val[u], tp[u]);
+#pragma unroll
+        for (int u = 0; u < S; ++u) {
+          tp[u] = dmul(cz, dsub(qs<L>(st, y + 1, x + 1, u), qc[u]));
+          val[u] = dadd(val[u], tp[u]);
+        }
+        // flux differences x, y, z (vectorized.py:193-200)
+        add_flux(val, inv,
+                 [&](int u) { return u == 0 ? qs<L>(stc, y + 1, x, 1) : xs_r[xs_at(u, y, x)]; },
+                 [&](int u) { return u == 0 ? qc[1] : xs_r[xs_at(u, y, x + 1)]; },
+                 [&](int u) { return u == 0 ? qs<L>(stc, y + 1, x + 2, 1) : xs_r[xs_at(u, y, x + 2)]; });
+        add_flux(val, inv,
+                 [&](int u) { return u == 0 ? qs<L>(stc, y, x + 1, 2) : ys_r[ys_at(u, y, x)]; },
+                 [&](int u) { return u == 0 ? qc[2] : ys_r[ys_at(u, y + 1, x)]; },
+                 [&](int u) { return u == 0 ? qs<L>(stc, y + 2, x + 1, 2) : ys_r[ys_at(u, y + 2, x)]; });
+        const double jz_up = qs<L>(st, y + 1, x + 1, 3);
+#pragma unroll
+        for (int u = 0; u < S; ++u) {
+          const double c = u == 0 ? qc[3] : zprev.f[u - 1];
+          const double favg_p = dmul(0.5, dadd(c, u == 0 ? jz_up : zcur.f[u - 1]));
+          val[u] = dadd(val[u], dmul(inv, dsub(favg_zm[u], favg_p)));
+          favg_zm[u] = favg_p;
+        }
+        // fix_negzero: the re-used z- term can only differ from the reference's
+        // in the sign of an exact zero, visible solely as a -0.0 result whose
+        // lower neighbour holds -0.0 in the same unknown (then the reference
+        // adds +0.0 and ends at +0.0).  Rare: check the input in HBM.
+        bool nz = false;
+#pragma unroll
+        for (int u = 0; u < S; ++u) nz = nz || is_negzero(val[u]);
+        if (__builtin_expect(nz, 0)) {
+          const int64_t vlow = ((int64_t)(zh - 2) * E + (y + 1)) * E + (x + 1);
+#pragma unroll
+          for (int u = 0; u < S; ++u) {
+            const double qlow = L == kAoS ? qin[(pidx * VOL + vlow) * S + u] : qin[((int64_t)u * n + pidx) * VOL + vlow];
+            if (is_negzero(val[u]) && is_negzero(qlow)) val[u] = 0.0;
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < S; ++u) {
+          if (L == kAoS) outb[(y * P + x) * S + u] = val[u];
+          else outb[u * P * P + y * P + x] = val[u];
+        }
+        fence_proxy_async();
+      } else {
+        // zh == 1: only the face (0 | 1) -- the minus face of the first interior plane
+#pragma unroll
+        for (int u = 0; u < S; ++u) {
+          const double qu = qs<L>(st, y + 1, x + 1, u);
+          tp[u] = dmul(cz, dsub(qu, qc[u]));
+          const double c = u == 0 ? qc[3] : zprev.f[u - 1];
+          favg_zm[u] = dmul(0.5, dadd(c, u == 0 ? qs<L>(st, y + 1, x + 1, 3) : zcur.f[u - 1]));
+        }
+      }
+    }
+    if (interior) {
+      zprev = zcur;
+      if (zh == NPL - 1) {   // patch complete: per-warp max of the wave speeds
+        unsigned long long m = cm;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          const unsigned long long v = __shfl_xor_sync(0xffffffffu, m, o);
+          m = v > m ? v : m;
+        }
+        if (lane == 0) wmax[((g / NPL) & 1) * 8 + warp] = m;
+        cm = 0;
+      }
+    }
+    __syncthreads();
+    if (producer && zh >= 2) store_out(g);
+  }
+
+  const int any_bad = __syncthreads_or(bad ? 1 : 0);
+  if (producer) {
+    if (G >= 1) finish_patch_max((G - 1) / NPL);
+    bulk_wait_all0();
+  }
+  if (tid == 0 && any_bad) atomicOr(status, 1u);
+}
+
+static int min_blocks_choice() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("FVB_FUSED_MINB");
+    v = (e && e[0] == '1') ? 1 : 2;
+  }
+  return v;
+}
+
+template <int L, int MINB>
+cudaError_t launch_impl(const FvbArgs& a, cudaStream_t st) {
+  auto kfn = fused3d_kernel<L, MINB>;
+  cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)BYTES);
+  if (e != cudaSuccess) return e;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  int per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kfn, 288, BYTES);
+  if (per_sm < 1) per_sm = 1;
+  int64_t grid = (int64_t)sms * per_sm;
+  if (grid > a.n) grid = a.n;
+  const Closure cl{a.gamma, a.gamma - 1.0};
+  kfn<<<(unsigned)grid, 288, BYTES, st>>>(a.qin, a.qout, a.cell_size, a.dt, a.max_eig, a.status, a.n, cl);
+  return cudaGetLastError();
+}
+
+}  // namespace f3
+}  // namespace fvb
+
+cudaError_t fvb_launch_fused3d16(const FvbArgs& a, cudaStream_t st) {
+  using namespace fvb;
+  if (a.n <= 0) return cudaSuccess;
+  const bool one = f3::min_blocks_choice() == 1;
+  if (a.layout == kAoS) return one ? f3::launch_impl<kAoS, 1>(a, st) : f3::launch_impl<kAoS, 2>(a, st);
+  return one ? f3::launch_impl<kSoA, 1>(a, st) : f3::launch_impl<kSoA, 2>(a, st);
+}

@@ -22,6 +22,8 @@ struct FvbArgs {
 
 cudaError_t fvb_launch_generic(const FvbArgs& a, cudaStream_t st);
 cudaError_t fvb_launch_fused16(const FvbArgs& a, cudaStream_t st);
+cudaError_t fvb_launch_fused3d16(const FvbArgs& a, cudaStream_t st);
+cudaError_t fvb_launch_redo(const FvbArgs& a, cudaStream_t st);
 bool fvb_fused16_supported(int dim, int p, int layout);
 cudaError_t fvb_launch_locate(int dim, int p, int64_t n, double gamma, int layout, const double* qin,
                               BoxInfo* info, cudaStream_t st);

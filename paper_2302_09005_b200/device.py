@@ -85,7 +85,8 @@ class DeviceBatch:
         self.cell_size = torch.ones(self.n_patches * d, **f64)
         self.dt = torch.zeros(self.n_patches, **f64)
         self.max_eigenvalue = torch.zeros(self.n_patches, **f64)
-        self.status = torch.zeros(4, dtype=torch.int32, device=self.device)
+        # status[0]: non-physical flag; status[1], status[2..]: redo list (include/fvb200.h)
+        self.status = torch.zeros(self.n_patches + 2, dtype=torch.int32, device=self.device)
 
     # -- construction / transfer ---------------------------------------------------------------
     @classmethod
