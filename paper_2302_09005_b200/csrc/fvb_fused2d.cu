@@ -165,7 +165,7 @@ fused2d_kernel(const double* __restrict__ qin, double* __restrict__ qout, const 
       load_q<L>(st, y + 1, x + 1, q);
       Side<2> sd[2];
       bool ok;
-      const Thermo<2> T = closure_all_fast<2>(q, cl, sd, ok);
+      const Thermo<2> T = closure_all_ranged<2>(q, cl, sd, ok);
       bad = bad || (ok && T.bad);
       if (!ok) atomicOr(&slowflag[g % 3], 1u);
       const unsigned long long a = (unsigned long long)__double_as_longlong(sd[0].lam);
@@ -180,7 +180,7 @@ fused2d_kernel(const double* __restrict__ qin, double* __restrict__ qout, const 
         load_q<L>(st, hy, x + 1, q);
         Side<2> sh;
         bool ok;
-        const Thermo<2> T = closure_one_fast<2>(q, cl, 1, sh, ok);
+        const Thermo<2> T = closure_one_ranged<2>(q, cl, 1, sh, ok);
         bad = bad || (ok && T.bad);
         if (!ok) atomicOr(&slowflag[g % 3], 1u);
         put_ys(ys_w, hy, x, sh);
@@ -191,7 +191,7 @@ fused2d_kernel(const double* __restrict__ qin, double* __restrict__ qout, const 
         load_q<L>(st, x + 1, hx, q);
         Side<2> sh;
         bool ok;
-        const Thermo<2> T = closure_one_fast<2>(q, cl, 0, sh, ok);
+        const Thermo<2> T = closure_one_ranged<2>(q, cl, 0, sh, ok);
         bad = bad || (ok && T.bad);
         if (!ok) atomicOr(&slowflag[g % 3], 1u);
         put_xs(xs_w, x, hx, sh);

@@ -215,7 +215,7 @@ fused3d_kernel(const double* __restrict__ qin, double* __restrict__ qout, const 
       if (full_plane) {
         Side<3> sd[3];
         bool ok;
-        const Thermo<3> T = closure_all_fast<3>(q, cl, sd, ok);
+        const Thermo<3> T = closure_all_ranged<3>(q, cl, sd, ok);
         bad = bad || (ok && T.bad);
         if (!ok) atomicOr(&slowflag[(g / NPL) & 1], 1u);
         unsigned long long m = (unsigned long long)__double_as_longlong(sd[0].lam);
@@ -229,7 +229,7 @@ fused3d_kernel(const double* __restrict__ qin, double* __restrict__ qout, const 
         zcur = sd[2];
       } else {
         bool ok;
-        const Thermo<3> T = closure_one_fast<3>(q, cl, 2, zcur, ok);
+        const Thermo<3> T = closure_one_ranged<3>(q, cl, 2, zcur, ok);
         bad = bad || (ok && T.bad);
         if (!ok) atomicOr(&slowflag[(g / NPL) & 1], 1u);
       }
@@ -240,7 +240,7 @@ fused3d_kernel(const double* __restrict__ qin, double* __restrict__ qout, const 
         load_q<L>(st, hy, x + 1, q);
         Side<3> sh;
         bool ok;
-        const Thermo<3> T = closure_one_fast<3>(q, cl, 1, sh, ok);
+        const Thermo<3> T = closure_one_ranged<3>(q, cl, 1, sh, ok);
         bad = bad || (ok && T.bad);
         if (!ok) atomicOr(&slowflag[(g / NPL) & 1], 1u);
         put_ys(ys_w, hy, x, sh);
@@ -251,7 +251,7 @@ fused3d_kernel(const double* __restrict__ qin, double* __restrict__ qout, const 
         load_q<L>(st, x + 1, hx, q);
         Side<3> sh;
         bool ok;
-        const Thermo<3> T = closure_one_fast<3>(q, cl, 0, sh, ok);
+        const Thermo<3> T = closure_one_ranged<3>(q, cl, 0, sh, ok);
         bad = bad || (ok && T.bad);
         if (!ok) atomicOr(&slowflag[(g / NPL) & 1], 1u);
         put_xs(xs_w, x, hx, sh);

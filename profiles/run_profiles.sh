@@ -13,7 +13,7 @@ ncu --metrics gpu__time_duration.sum --clock-control none --csv \
     python bench.py --config ${CFG} --layout ${LAYOUT} --steps 5 --warmup 3 --e2e-steps 0 --no-cpu-baseline \
     > ${OUT}_launches.log 2>&1
 # one full capture of the fused update kernel (skip the first launches)
-ncu --set full --clock-control none --import-source on -k regex:fused16 -s 2 -c 1 \
+ncu --set full --clock-control none --import-source on -k regex:fused -s 2 -c 1 \
     -o ${OUT}_full -f \
     python bench.py --config ${CFG} --layout ${LAYOUT} --steps 3 --warmup 3 --e2e-steps 0 --no-cpu-baseline \
     > ${OUT}_full.log 2>&1
