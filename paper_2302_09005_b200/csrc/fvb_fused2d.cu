@@ -43,7 +43,8 @@ constexpr int OFF_YS = OFF_RING + NST * STAGE;
 constexpr int OFF_XS = OFF_YS + 2 * SIDE;
 constexpr int OFF_OUT = OFF_XS + 2 * SIDE;
 constexpr int OFF_WMAX = OFF_OUT + 2 * OUTN;
-constexpr int OFF_FLAG = OFF_WMAX + 16;
+constexpr int OFF_INV = OFF_WMAX + 16;      // (inv, half_inv) per patch parity
+constexpr int OFF_FLAG = OFF_INV + 4;
 constexpr int OFF_BAR = OFF_FLAG + 2;   // 3 flag words (4 B) fit in 2 doubles
 constexpr int TOTAL = OFF_BAR + NST;
 constexpr size_t BYTES = (size_t)TOTAL * 8;
@@ -82,6 +83,7 @@ fused2d_kernel(const double* __restrict__ qin, double* __restrict__ qout, const 
   double* xsb = sm + OFF_XS;
   double* outb = sm + OFF_OUT;
   unsigned long long* wmax = reinterpret_cast<unsigned long long*>(sm + OFF_WMAX);
+  double* invs = sm + OFF_INV;
   unsigned* slowflag = reinterpret_cast<unsigned*>(sm + OFF_FLAG);
   uint64_t* bars = reinterpret_cast<uint64_t*>(sm + OFF_BAR);
 
@@ -92,10 +94,10 @@ fused2d_kernel(const double* __restrict__ qin, double* __restrict__ qout, const 
   const int y = ((warp & 7) << 1) | (lane >> 4);
   const bool producer = tid == 256;
 
-  const int64_t G = (n > (int64_t)blockIdx.x) ? (n - 1 - (int64_t)blockIdx.x) / gridDim.x + 1 : 0;
-  auto patch_of = [&](int64_t g) -> int64_t { return (int64_t)blockIdx.x + g * (int64_t)gridDim.x; };
+  const int G = (n > (int64_t)blockIdx.x) ? (int)((n - 1 - (int64_t)blockIdx.x) / gridDim.x + 1) : 0;
+  auto patch_of = [&](int g) -> int64_t { return (int64_t)blockIdx.x + (int64_t)g * gridDim.x; };
 
-  auto issue = [&](int64_t g) {
+  auto issue = [&](int g) {
     const int64_t pidx = patch_of(g);
     double* st = ring + (g % NST) * STAGE;
     uint64_t* bar = bars + (g % NST);
@@ -109,7 +111,7 @@ fused2d_kernel(const double* __restrict__ qin, double* __restrict__ qout, const 
         tma_load_1d(st + u * PLANE, qin + ((int64_t)u * n + pidx) * VOL, (uint32_t)(PLANE * 8), bar);
     }
   };
-  auto store_out = [&](int64_t g) {
+  auto store_out = [&](int g) {
     const int64_t pidx = patch_of(g);
     const double* src = outb + (g & 1) * OUTN;
     if (L == kAoS) {
@@ -121,7 +123,7 @@ fused2d_kernel(const double* __restrict__ qin, double* __restrict__ qout, const 
     }
     bulk_commit();
   };
-  auto finish_patch = [&](int64_t g) {
+  auto finish_patch = [&](int g) {
     unsigned long long m = wmax[(g & 1) * 8];
 #pragma unroll
     for (int w = 1; w < 8; ++w) {
@@ -144,17 +146,25 @@ fused2d_kernel(const double* __restrict__ qin, double* __restrict__ qout, const 
     fence_mbar_init();
   }
   __syncthreads();
-  if (producer)
-    for (int64_t g = 0; g < NST && g < G; ++g) issue(g);
+  // dt / dx of a patch, computed once by the producer (vectorized.py:169-170)
+  auto put_inv = [&](int g) {
+    const int64_t pi = patch_of(g);
+    const double dx = __ddiv_rn(cell_size[pi * 2], (double)P);
+    const double inv = __ddiv_rn(dtv[pi], dx);
+    invs[(g & 1) * 2] = inv;
+    invs[(g & 1) * 2 + 1] = dmul(0.5, inv);   // `0.5 * inv * a` evaluates 0.5*inv first
+  };
+  if (producer) {
+    for (int g = 0; g < NST && g < G; ++g) issue(g);
+    if (G > 0) put_inv(0);
+  }
 
   bool bad = false;
-  for (int64_t g = 0; g < G; ++g) {
-    const int64_t pidx = patch_of(g);
-    const double dx = __ddiv_rn(cell_size[pidx * 2], (double)P);   // vectorized.py:169
-    const double inv = __ddiv_rn(dtv[pidx], dx);                     // vectorized.py:170
-    const double half_inv = dmul(0.5, inv);                          // `0.5 * inv * a`
-    const double* st = ring + (g % NST) * STAGE;
-    mbar_wait(&bars[g % NST], (uint32_t)((g / NST) & 1));
+  int64_t pidx = blockIdx.x;
+  unsigned stg = 0, par = 0, slot3 = 0;   // ring stage / mbarrier parity / g % 3, advanced incrementally
+  for (int g = 0; g < G; ++g) {
+    const double* st = ring + stg * STAGE;
+    mbar_wait(&bars[stg], par);
     double* ys_w = ysb + (g & 1) * SIDE;
     double* xs_w = xsb + (g & 1) * SIDE;
 
@@ -167,7 +177,7 @@ fused2d_kernel(const double* __restrict__ qin, double* __restrict__ qout, const 
       bool ok;
       const Thermo<2> T = closure_all_ranged<2>(q, cl, sd, ok);
       bad = bad || (ok && T.bad);
-      if (!ok) atomicOr(&slowflag[g % 3], 1u);
+      if (!ok) atomicOr(&slowflag[slot3], 1u);
       const unsigned long long a = (unsigned long long)__double_as_longlong(sd[0].lam);
       const unsigned long long b = (unsigned long long)__double_as_longlong(sd[1].lam);
       cmax = a > b ? a : b;
@@ -182,7 +192,7 @@ fused2d_kernel(const double* __restrict__ qin, double* __restrict__ qout, const 
         bool ok;
         const Thermo<2> T = closure_one_ranged<2>(q, cl, 1, sh, ok);
         bad = bad || (ok && T.bad);
-        if (!ok) atomicOr(&slowflag[g % 3], 1u);
+        if (!ok) atomicOr(&slowflag[slot3], 1u);
         put_ys(ys_w, hy, x, sh);
       }
       {   // x-face halo columns (haloed x = 0, 17)
@@ -193,7 +203,7 @@ fused2d_kernel(const double* __restrict__ qin, double* __restrict__ qout, const 
         bool ok;
         const Thermo<2> T = closure_one_ranged<2>(q, cl, 0, sh, ok);
         bad = bad || (ok && T.bad);
-        if (!ok) atomicOr(&slowflag[g % 3], 1u);
+        if (!ok) atomicOr(&slowflag[slot3], 1u);
         put_xs(xs_w, x, hx, sh);
       }
     }
@@ -205,10 +215,12 @@ fused2d_kernel(const double* __restrict__ qin, double* __restrict__ qout, const 
         store_out(g - 1);
         finish_patch(g - 1);
       }
+      if (g + 1 < G) put_inv(g + 1);   // read after the next barrier
     }
 
     // ---------------- B: face terms and update ----------------
     if (interior) {
+      const double inv = invs[(g & 1) * 2], half_inv = invs[(g & 1) * 2 + 1];
       double qc[S], qn[S], val[S];
       load_q<L>(st, y + 1, x + 1, qc);
 #pragma unroll
@@ -251,6 +263,10 @@ fused2d_kernel(const double* __restrict__ qin, double* __restrict__ qout, const 
       }
       if (lane == 0) wmax[(g & 1) * 8 + warp] = cmax;
     }
+    pidx += gridDim.x;
+    stg = (stg + 1) & (NST - 1);
+    par ^= (stg == 0);
+    slot3 = slot3 == 2 ? 0 : slot3 + 1;
   }
 
   const int any_bad = __syncthreads_or(bad ? 1 : 0);

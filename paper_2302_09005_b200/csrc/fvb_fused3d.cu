@@ -121,13 +121,13 @@ fused3d_kernel(const double* __restrict__ qin, double* __restrict__ qout, const 
   const int y = ((warp & 7) << 1) | (lane >> 4);
   const bool producer = tid == 256;
 
-  const int64_t my_patches = (n > (int64_t)blockIdx.x) ? (n - 1 - (int64_t)blockIdx.x) / gridDim.x + 1 : 0;
-  const int64_t G = my_patches * NPL;
-  auto patch_of = [&](int64_t g) -> int64_t { return (int64_t)blockIdx.x + (g / NPL) * (int64_t)gridDim.x; };
+  const int my_patches = (n > (int64_t)blockIdx.x) ? (int)((n - 1 - (int64_t)blockIdx.x) / gridDim.x + 1) : 0;
+  const int G = my_patches * NPL;   // planes this CTA streams (iteration count)
+  auto patch_of = [&](int g) -> int64_t { return (int64_t)blockIdx.x + (int64_t)(g / NPL) * gridDim.x; };
 
-  auto issue = [&](int64_t g) {
+  auto issue = [&](int g) {
     const int64_t pidx = patch_of(g);
-    const int zh = (int)(g % NPL);
+    const int zh = g % NPL;
     double* st = ring + (g % NST) * STAGE;
     uint64_t* bar = bars + (g % NST);
     fence_proxy_async();
@@ -141,9 +141,9 @@ fused3d_kernel(const double* __restrict__ qin, double* __restrict__ qout, const 
                     (uint32_t)(PLANE * 8), bar);
     }
   };
-  auto store_out = [&](int64_t g) {   // output of iteration g: interior plane zh-2
+  auto store_out = [&](int g) {   // output of iteration g: interior plane zh-2
     const int64_t pidx = patch_of(g);
-    const int z = (int)(g % NPL) - 2;
+    const int z = g % NPL - 2;
     if (L == kAoS) {
       tma_store_1d(qout + (pidx * IVOL + (int64_t)z * P * P) * S, outb, (uint32_t)(OUTN * 8));
     } else {
@@ -154,14 +154,14 @@ fused3d_kernel(const double* __restrict__ qin, double* __restrict__ qout, const 
     }
     bulk_commit();
   };
-  auto finish_patch_max = [&](int64_t j) {
+  auto finish_patch_max = [&](int j) {
     unsigned long long m = wmax[(j & 1) * 8];
 #pragma unroll
     for (int w = 1; w < 8; ++w) {
       const unsigned long long v = wmax[(j & 1) * 8 + w];
       m = v > m ? v : m;
     }
-    const int64_t pidx = (int64_t)blockIdx.x + j * (int64_t)gridDim.x;
+    const int64_t pidx = (int64_t)blockIdx.x + (int64_t)j * gridDim.x;
     max_eig[pidx] = __longlong_as_double((long long)m);
     if (slowflag[j & 1]) {   // queue the patch for the exact re-evaluation (fvb_redo_kernel)
       const unsigned k = atomicAdd(&status[1], 1u);
@@ -178,7 +178,7 @@ fused3d_kernel(const double* __restrict__ qin, double* __restrict__ qout, const 
   }
   __syncthreads();
   if (producer)
-    for (int64_t g = 0; g < 2 && g < G; ++g) issue(g);
+    for (int g = 0; g < 2 && g < G; ++g) issue(g);
 
   bool bad = false;
   unsigned long long cm = 0;   // running max wave speed (bit pattern) of this column
@@ -193,16 +193,18 @@ fused3d_kernel(const double* __restrict__ qin, double* __restrict__ qout, const 
 #pragma unroll
   for (int k = 0; k < 4; ++k) zprev.f[k] = 0.0;
 
-  for (int64_t g = 0; g < G; ++g) {
-    const int zh = (int)(g % NPL);
-    const int64_t pidx = patch_of(g);
+  // per-iteration indices advanced incrementally (no 64-bit div/mod in the loop)
+  int zh = 0, jp = 0;                  // plane within the patch, patch ordinal of this CTA
+  int64_t pidx = blockIdx.x;           // patch index
+  unsigned stg = 0, par = 0;           // ring stage of plane g and its mbarrier parity
+  for (int g = 0; g < G; ++g) {
     if (zh == 0) {
       const double dx = __ddiv_rn(cell_size[pidx * 3], (double)P);   // vectorized.py:169
       inv = __ddiv_rn(dtv[pidx], dx);                                  // vectorized.py:170
       half_inv = dmul(0.5, inv);                                       // `0.5 * inv * a`
     }
-    const double* st = ring + (g % NST) * STAGE;
-    mbar_wait(&bars[g % NST], (uint32_t)((g / NST) & 1));
+    const double* st = ring + stg * STAGE;
+    mbar_wait(&bars[stg], par);
     const bool full_plane = zh >= 1 && zh <= P;
     double* ys_w = ysb + (g & 1) * SIDE;
     double* xs_w = xsb + (g & 1) * SIDE;
@@ -217,7 +219,7 @@ fused3d_kernel(const double* __restrict__ qin, double* __restrict__ qout, const 
         bool ok;
         const Thermo<3> T = closure_all_ranged<3>(q, cl, sd, ok);
         bad = bad || (ok && T.bad);
-        if (!ok) atomicOr(&slowflag[(g / NPL) & 1], 1u);
+        if (!ok) atomicOr(&slowflag[jp & 1], 1u);
         unsigned long long m = (unsigned long long)__double_as_longlong(sd[0].lam);
         unsigned long long v = (unsigned long long)__double_as_longlong(sd[1].lam);
         m = v > m ? v : m;
@@ -231,7 +233,7 @@ fused3d_kernel(const double* __restrict__ qin, double* __restrict__ qout, const 
         bool ok;
         const Thermo<3> T = closure_one_ranged<3>(q, cl, 2, zcur, ok);
         bad = bad || (ok && T.bad);
-        if (!ok) atomicOr(&slowflag[(g / NPL) & 1], 1u);
+        if (!ok) atomicOr(&slowflag[jp & 1], 1u);
       }
     } else if (full_plane) {
       {   // y-face halo rows (haloed y = 0, 17), interior columns
@@ -242,7 +244,7 @@ fused3d_kernel(const double* __restrict__ qin, double* __restrict__ qout, const 
         bool ok;
         const Thermo<3> T = closure_one_ranged<3>(q, cl, 1, sh, ok);
         bad = bad || (ok && T.bad);
-        if (!ok) atomicOr(&slowflag[(g / NPL) & 1], 1u);
+        if (!ok) atomicOr(&slowflag[jp & 1], 1u);
         put_ys(ys_w, hy, x, sh);
       }
       {   // x-face halo columns (haloed x = 0, 17), interior rows
@@ -253,7 +255,7 @@ fused3d_kernel(const double* __restrict__ qin, double* __restrict__ qout, const 
         bool ok;
         const Thermo<3> T = closure_one_ranged<3>(q, cl, 0, sh, ok);
         bad = bad || (ok && T.bad);
-        if (!ok) atomicOr(&slowflag[(g / NPL) & 1], 1u);
+        if (!ok) atomicOr(&slowflag[jp & 1], 1u);
         put_xs(xs_w, x, hx, sh);
       }
     }
@@ -261,12 +263,12 @@ fused3d_kernel(const double* __restrict__ qin, double* __restrict__ qout, const 
     __syncthreads();
     if (producer) {
       if (g + 2 < G) issue(g + 2);    // into the stage of plane g-2, unused from here on
-      if (g >= 1 && (g - 1) % NPL == NPL - 1) finish_patch_max((g - 1) / NPL);
+      if (zh == 0 && jp >= 1) finish_patch_max(jp - 1);
     }
 
     // ---------------- B: update of the cells of plane zh-1 ----------------
     if (interior && zh >= 1) {
-      const double* stc = ring + ((g + NST - 1) % NST) * STAGE;   // plane zh-1
+      const double* stc = ring + ((stg + NST - 1) & (NST - 1)) * STAGE;   // plane zh-1
       const double* ys_r = ysb + ((g - 1) & 1) * SIDE;
       const double* xs_r = xsb + ((g - 1) & 1) * SIDE;
       double qc[S], val[S], qn[S];
@@ -353,12 +355,19 @@ fused3d_kernel(const double* __restrict__ qin, double* __restrict__ qout, const 
           const unsigned long long v = __shfl_xor_sync(0xffffffffu, m, o);
           m = v > m ? v : m;
         }
-        if (lane == 0) wmax[((g / NPL) & 1) * 8 + warp] = m;
+        if (lane == 0) wmax[(jp & 1) * 8 + warp] = m;
         cm = 0;
       }
     }
     __syncthreads();
     if (producer && zh >= 2) store_out(g);
+    stg = (stg + 1) & (NST - 1);
+    par ^= (stg == 0);
+    if (++zh == NPL) {
+      zh = 0;
+      ++jp;
+      pidx += gridDim.x;
+    }
   }
 
   const int any_bad = __syncthreads_or(bad ? 1 : 0);
