@@ -116,15 +116,19 @@ def cpu_cores() -> int:
         return os.cpu_count() or 1
 
 
-def run_cpu_sample(dim: int, p: int, target_s: float = 8.0):
+def run_cpu_sample(dim: int, p: int, target_s: float | None = None):
     """Time the oracle port on a bounded sample of the workload; returns (cells/s, cores, description)."""
     import numpy as np
 
     import oracle
 
     oracle.build()
+    if target_s is None:
+        target_s = float(os.environ.get("FVB_BENCH_CPU_SECONDS", "8"))
     cores = cpu_cores()
     n = max(cores * 4, 64) if p >= 16 else max(cores * 256, 4096)
+    if os.environ.get("FVB_BENCH_CPU_SMALL"):   # CI: a tiny sample
+        n = max(cores, 2)
     qin = oracle.synthetic_qin(dim, p, n, seed=7)
     cs = np.ones((n, dim))
     dt = np.full(n, 0.4 * (1.0 / p) / 3.4)
@@ -146,10 +150,11 @@ def reference_arm(args):
     dim, p, n_per_gpu, _ = CONFIGS[args.config]
     per_step = []
     value_total, cores, desc = None, None, None
+    budget = float(os.environ.get("FVB_BENCH_CPU_SECONDS", "20"))
     for _ in range(args.warmup):
-        run_cpu_sample(dim, p, target_s=1.0)
+        run_cpu_sample(dim, p, target_s=min(1.0, budget / 10))
     for _ in range(args.steps):
-        v, cores, desc = run_cpu_sample(dim, p, target_s=max(1.0, 20.0 / max(args.steps, 1)))
+        v, cores, desc = run_cpu_sample(dim, p, target_s=max(budget / max(args.steps, 1), 0.05))
         per_step.append(v)
     value_total = statistics.median(per_step)
     line = {

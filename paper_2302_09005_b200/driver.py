@@ -23,6 +23,18 @@ from . import _lib
 from .device import DeviceBatch, _stream_handle, _torch, _vp
 
 
+def allreduce_max_(t, group=None):
+    """In-place MAX all-reduce of the wave speed across ranks (the step's only exchange).
+
+    NCCL over NVLink on the GPU ranks; any backend works (the CPU tests use gloo).
+    A no-op for a single process."""
+    import torch.distributed as dist
+
+    if dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX, group=group)
+    return t
+
+
 def shard_bounds(n: int, rank: int, world: int) -> tuple[int, int]:
     """Contiguous patch range of a rank (preserves the global patch order)."""
     base, extra = divmod(n, world)
@@ -58,7 +70,7 @@ class CflStepper:
             return
         _lib.check(L.fvb_reduce_dt(_vp(self.db.max_eigenvalue), self.db.n_patches, self.cfl, self.dx,
                                    _vp(self.gmax), None, None, 0, st), "fvb_reduce_dt")
-        self._dist.all_reduce(self.gmax, op=self._dist.ReduceOp.MAX, group=self.group)
+        allreduce_max_(self.gmax, self.group)
         _lib.check(L.fvb_set_dt(_vp(self.gmax), self.cfl, self.dx, _vp(self.dt_scalar), _vp(self.db.dt),
                                 self.db.n_patches, st), "fvb_set_dt")
 
