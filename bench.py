@@ -339,7 +339,8 @@ def main():
                          "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_kind})"},
             "cpu_baseline": cpu,
             "e2e": e2e,
-            "gpu_launches": args.steps * 3,
+            # per step: the update kernel (+ the fused path's redo pass) + reduce_max + set_dt
+            "gpu_launches": args.steps * ((2 if kernel_name == "fused" else 1) + 2),
             "clocks": clocks.summary(),
         }
         print(json.dumps(line), flush=True)
