@@ -3,24 +3,27 @@
 // One persistent CTA (8 "interior" warps + 1 "halo" warp, 2 CTAs per SM)
 // marches each patch plane by plane in z:
 //
-//   ring    4 TMA bulk-copy stages of one haloed z-plane (18x18x5 doubles,
-//           12,960 B), mbarrier complete_tx; plane g+2 is issued while plane g
-//           is consumed.
+//   ring    3 TMA bulk-copy stages of one haloed z-plane (18x18x5 doubles,
+//           12,960 B), mbarrier complete_tx; plane g+2 is issued as soon as
+//           plane g-1 retires.
 //   xs, ys  x- and y-side data (lam, f[1..4]) of every volume of the plane,
 //           including the face-halo columns / rows (written by the halo
 //           warp), double-buffered by plane parity.
-//   ostage  one output plane (16x16x5) stored back with a TMA bulk store.
+//   ostage  two output planes (16x16x5) stored back with TMA bulk stores.
 //
-// Iteration g (haloed plane zh):
+// Iteration g (haloed plane zh), ONE CTA barrier:
 //   A  interior lanes evaluate the Euler closure of their volume of plane zh
 //      once (14 quotients sharing one reciprocal refinement, fvb_exact.cuh)
 //      and publish its x/y-side data; the halo warp publishes the x/y face
-//      halo volumes.                                             -- barrier
-//   B  interior lanes update their cell of plane zh-1 from the published
-//      side data (x and y faces evaluated from both sides, exactly as the
-//      reference's per-volume passes), and the z faces marching in
-//      registers: the face (zh-1 | zh) is evaluated once and re-used, negated,
-//      as the minus face of the next plane.                      -- barrier
+//      halo volumes of plane zh.
+//   B  interior lanes update their cell of plane zh-1 from the side data
+//      published in the previous iteration (x and y faces evaluated from both
+//      sides, exactly as the reference's per-volume passes) and the z faces
+//      marching in registers: the face (zh-1 | zh) is evaluated once and
+//      re-used, negated, as the minus face of the next plane.  -- barrier
+//   A(g) and B(g) touch disjoint buffers, so they need no barrier between
+//   them; the barrier after B(g) orders A(g) before B(g+1) and B(g) before
+//   A(g+2)'s reuse of the same parity.
 //
 // The re-used z face is the only place the arithmetic is not literally the
 // reference's: -RN(c*(a-b)) equals RN(c*(b-a)) except for the sign of an
@@ -43,7 +46,7 @@ using namespace f16;
 constexpr int P = 16, E = 18, S = 5;
 constexpr int PLANE = E * E;              // haloed volumes per plane
 constexpr int STAGE = PLANE * S;          // doubles per ring stage
-constexpr int NST = 4;
+constexpr int NST = 3;   // planes g-1 and g are read in iteration g; g+1 is in flight
 constexpr int NPL = E;                    // planes per patch
 constexpr int64_t VOL = (int64_t)E * E * E;
 constexpr int64_t IVOL = (int64_t)P * P * P;
@@ -53,7 +56,7 @@ constexpr int OFF_RING = 0;
 constexpr int OFF_YS = OFF_RING + NST * STAGE;
 constexpr int OFF_XS = OFF_YS + 2 * SIDE;
 constexpr int OFF_OUT = OFF_XS + 2 * SIDE;
-constexpr int OFF_WMAX = OFF_OUT + OUTN;
+constexpr int OFF_WMAX = OFF_OUT + 2 * OUTN;   // output planes double-buffered
 constexpr int OFF_FLAG = OFF_WMAX + 16;
 constexpr int OFF_BAR = OFF_FLAG + 1;
 constexpr int TOTAL = OFF_BAR + NST;
@@ -141,15 +144,16 @@ fused3d_kernel(const double* __restrict__ qin, double* __restrict__ qout, const 
                     (uint32_t)(PLANE * 8), bar);
     }
   };
-  auto store_out = [&](int g) {   // output of iteration g: interior plane zh-2
+  auto store_out = [&](int g) {   // output of iteration g: interior plane zh-2, buffer g & 1
     const int64_t pidx = patch_of(g);
     const int z = g % NPL - 2;
+    const double* src = outb + (g & 1) * OUTN;
     if (L == kAoS) {
-      tma_store_1d(qout + (pidx * IVOL + (int64_t)z * P * P) * S, outb, (uint32_t)(OUTN * 8));
+      tma_store_1d(qout + (pidx * IVOL + (int64_t)z * P * P) * S, src, (uint32_t)(OUTN * 8));
     } else {
 #pragma unroll
       for (int u = 0; u < S; ++u)
-        tma_store_1d(qout + ((int64_t)u * n + pidx) * IVOL + (int64_t)z * P * P, outb + u * P * P,
+        tma_store_1d(qout + ((int64_t)u * n + pidx) * IVOL + (int64_t)z * P * P, src + u * P * P,
                      (uint32_t)(P * P * 8));
     }
     bulk_commit();
@@ -259,16 +263,13 @@ fused3d_kernel(const double* __restrict__ qin, double* __restrict__ qout, const 
         put_xs(xs_w, x, hx, sh);
       }
     }
-    if (producer) bulk_wait_read0();   // ostage read by its TMA store
-    __syncthreads();
-    if (producer) {
-      if (g + 2 < G) issue(g + 2);    // into the stage of plane g-2, unused from here on
-      if (zh == 0 && jp >= 1) finish_patch_max(jp - 1);
-    }
+    // No barrier here: the update below reads plane zh-1's side data (published
+    // last iteration, behind the barrier that ended it) and this column's own
+    // plane-zh z data.
 
     // ---------------- B: update of the cells of plane zh-1 ----------------
     if (interior && zh >= 1) {
-      const double* stc = ring + ((stg + NST - 1) & (NST - 1)) * STAGE;   // plane zh-1
+      const double* stc = ring + (stg == 0 ? NST - 1 : stg - 1) * STAGE;   // plane zh-1
       const double* ys_r = ysb + ((g - 1) & 1) * SIDE;
       const double* xs_r = xsb + ((g - 1) & 1) * SIDE;
       double qc[S], val[S], qn[S];
@@ -330,9 +331,11 @@ fused3d_kernel(const double* __restrict__ qin, double* __restrict__ qout, const 
           }
         }
 #pragma unroll
+        double* ob = outb + (g & 1) * OUTN;
+#pragma unroll
         for (int u = 0; u < S; ++u) {
-          if (L == kAoS) outb[(y * P + x) * S + u] = val[u];
-          else outb[u * P * P + y * P + x] = val[u];
+          if (L == kAoS) ob[(y * P + x) * S + u] = val[u];
+          else ob[u * P * P + y * P + x] = val[u];
         }
         fence_proxy_async();
       } else {
@@ -359,9 +362,16 @@ fused3d_kernel(const double* __restrict__ qin, double* __restrict__ qout, const 
         cm = 0;
       }
     }
+    // One barrier per plane: publishes this plane's side data and output, and
+    // retires plane zh-1's stage and side buffers for reuse.
+    if (producer) bulk_wait_read0();   // output buffer (g+1)&1, written next iteration, is free
     __syncthreads();
-    if (producer && zh >= 2) store_out(g);
-    stg = (stg + 1) & (NST - 1);
+    if (producer) {
+      if (g + 2 < G) issue(g + 2);     // into the stage of plane g-1, retired just now
+      if (zh >= 2) store_out(g);
+      if (zh == NPL - 1) finish_patch_max(jp);
+    }
+    stg = stg == NST - 1 ? 0 : stg + 1;
     par ^= (stg == 0);
     if (++zh == NPL) {
       zh = 0;
@@ -371,10 +381,7 @@ fused3d_kernel(const double* __restrict__ qin, double* __restrict__ qout, const 
   }
 
   const int any_bad = __syncthreads_or(bad ? 1 : 0);
-  if (producer) {
-    if (G >= 1) finish_patch_max((G - 1) / NPL);
-    bulk_wait_all0();
-  }
+  if (producer) bulk_wait_all0();
   if (tid == 0 && any_bad) atomicOr(status, 1u);
 }
 
