@@ -154,129 +154,132 @@ fused2d_kernel(const double* __restrict__ qin, double* __restrict__ qout, const 
     invs[(g & 1) * 2] = inv;
     invs[(g & 1) * 2 + 1] = dmul(0.5, inv);   // `0.5 * inv * a` evaluates 0.5*inv first
   };
-  if (producer) {
-    for (int g = 0; g < NST && g < G; ++g) issue(g);
-    if (G > 0) put_inv(0);
-  }
+  if (producer)
+    for (int g = 0; g < NST - 1 && g < G; ++g) issue(g);
 
   bool bad = false;
-  int64_t pidx = blockIdx.x;
-  unsigned stg = 0, par = 0, slot3 = 0;   // ring stage / mbarrier parity / g % 3, advanced incrementally
-  for (int g = 0; g < G; ++g) {
-    const double* st = ring + stg * STAGE;
-    mbar_wait(&bars[stg], par);
-    double* ys_w = ysb + (g & 1) * SIDE;
-    double* xs_w = xsb + (g & 1) * SIDE;
-
-    // ---------------- A: closures ----------------
-    unsigned long long cmax = 0;
-    if (interior) {
-      double q[S];
-      load_q<L>(st, y + 1, x + 1, q);
-      Side<2> sd[2];
-      bool ok;
-      const Thermo<2> T = closure_all_ranged<2>(q, cl, sd, ok);
-      bad = bad || (ok && T.bad);
-      if (!ok) atomicOr(&slowflag[slot3], 1u);
-      const unsigned long long a = (unsigned long long)__double_as_longlong(sd[0].lam);
-      const unsigned long long b = (unsigned long long)__double_as_longlong(sd[1].lam);
-      cmax = a > b ? a : b;
-      put_xs(xs_w, y, x + 1, sd[0]);
-      put_ys(ys_w, y + 1, x, sd[1]);
-    } else {
-      {   // y-face halo rows (haloed y = 0, 17)
-        const int hy = lane < 16 ? 0 : E - 1;
+  unsigned long long cmax = 0;            // this lane's wave speed of the patch in flight
+  unsigned stg = 0, par = 0, slot3 = 0;   // ring stage / mbarrier parity / g % 3 of patch g
+  // Software pipeline, ONE CTA barrier per patch: iteration g evaluates the
+  // closures of patch g (A) and updates patch g-1 (B) from the side data
+  // published in iteration g-1.  A(g) and B(g) touch different parities.
+  for (int g = 0; g <= G; ++g) {
+    const unsigned pstg = stg == 0 ? NST - 1 : stg - 1;   // stage of patch g-1
+    // ---------------- A: closures of patch g ----------------
+    unsigned long long cnew = 0;
+    if (g < G) {
+      const double* st = ring + stg * STAGE;
+      mbar_wait(&bars[stg], par);
+      double* ys_w = ysb + (g & 1) * SIDE;
+      double* xs_w = xsb + (g & 1) * SIDE;
+      if (interior) {
         double q[S];
-        load_q<L>(st, hy, x + 1, q);
-        Side<2> sh;
+        load_q<L>(st, y + 1, x + 1, q);
+        Side<2> sd[2];
         bool ok;
-        const Thermo<2> T = closure_one_ranged<2>(q, cl, 1, sh, ok);
+        const Thermo<2> T = closure_all_ranged<2>(q, cl, sd, ok);
         bad = bad || (ok && T.bad);
         if (!ok) atomicOr(&slowflag[slot3], 1u);
-        put_ys(ys_w, hy, x, sh);
-      }
-      {   // x-face halo columns (haloed x = 0, 17)
-        const int hx = lane < 16 ? 0 : E - 1;
-        double q[S];
-        load_q<L>(st, x + 1, hx, q);
-        Side<2> sh;
-        bool ok;
-        const Thermo<2> T = closure_one_ranged<2>(q, cl, 0, sh, ok);
-        bad = bad || (ok && T.bad);
-        if (!ok) atomicOr(&slowflag[slot3], 1u);
-        put_xs(xs_w, x, hx, sh);
+        const unsigned long long a = (unsigned long long)__double_as_longlong(sd[0].lam);
+        const unsigned long long b = (unsigned long long)__double_as_longlong(sd[1].lam);
+        cnew = a > b ? a : b;
+        put_xs(xs_w, y, x + 1, sd[0]);
+        put_ys(ys_w, y + 1, x, sd[1]);
+      } else {
+        {   // y-face halo rows (haloed y = 0, 17)
+          const int hy = lane < 16 ? 0 : E - 1;
+          double q[S];
+          load_q<L>(st, hy, x + 1, q);
+          Side<2> sh;
+          bool ok;
+          const Thermo<2> T = closure_one_ranged<2>(q, cl, 1, sh, ok);
+          bad = bad || (ok && T.bad);
+          if (!ok) atomicOr(&slowflag[slot3], 1u);
+          put_ys(ys_w, hy, x, sh);
+        }
+        {   // x-face halo columns (haloed x = 0, 17)
+          const int hx = lane < 16 ? 0 : E - 1;
+          double q[S];
+          load_q<L>(st, x + 1, hx, q);
+          Side<2> sh;
+          bool ok;
+          const Thermo<2> T = closure_one_ranged<2>(q, cl, 0, sh, ok);
+          bad = bad || (ok && T.bad);
+          if (!ok) atomicOr(&slowflag[slot3], 1u);
+          put_xs(xs_w, x, hx, sh);
+        }
+        if (producer) put_inv(g);   // read by B(g+1), behind this iteration's barrier
       }
     }
-    if (producer) bulk_wait_read0();   // output buffer (g & 1) free again
-    __syncthreads();
-    if (producer) {
-      if (g >= 1 && g + NST - 1 < G) issue(g + NST - 1);   // into the stage of patch g-1
-      if (g >= 1) {
-        store_out(g - 1);
-        finish_patch(g - 1);
-      }
-      if (g + 1 < G) put_inv(g + 1);   // read after the next barrier
-    }
-
-    // ---------------- B: face terms and update ----------------
-    if (interior) {
-      const double inv = invs[(g & 1) * 2], half_inv = invs[(g & 1) * 2 + 1];
+    // ---------------- B: update of patch g-1 ----------------
+    if (interior && g >= 1) {
+      const int gp = g - 1;
+      const double* st = ring + pstg * STAGE;
+      const double* ys_r = ysb + (gp & 1) * SIDE;
+      const double* xs_r = xsb + (gp & 1) * SIDE;
+      const double inv = invs[(gp & 1) * 2], half_inv = invs[(gp & 1) * 2 + 1];
       double qc[S], qn[S], val[S];
       load_q<L>(st, y + 1, x + 1, qc);
 #pragma unroll
       for (int u = 0; u < S; ++u) val[u] = qc[u];                       // _pass_copy
-      const double lx = xs_w[xs_at(0, y, x + 1)];
+      const double lx = xs_r[xs_at(0, y, x + 1)];
       load_q<L>(st, y + 1, x, qn);
-      dissipate<2>(val, half_inv, lx, qc, xs_w[xs_at(0, y, x)], qn);
+      const double jl = qn[1];
+      dissipate<2>(val, half_inv, lx, qc, xs_r[xs_at(0, y, x)], qn);
       load_q<L>(st, y + 1, x + 2, qn);
-      dissipate<2>(val, half_inv, lx, qc, xs_w[xs_at(0, y, x + 2)], qn);
-      const double ly = ys_w[ys_at(0, y + 1, x)];
+      const double jr = qn[1];
+      dissipate<2>(val, half_inv, lx, qc, xs_r[xs_at(0, y, x + 2)], qn);
+      const double ly = ys_r[ys_at(0, y + 1, x)];
       load_q<L>(st, y, x + 1, qn);
-      dissipate<2>(val, half_inv, ly, qc, ys_w[ys_at(0, y, x)], qn);
+      const double jd = qn[2];
+      dissipate<2>(val, half_inv, ly, qc, ys_r[ys_at(0, y, x)], qn);
       load_q<L>(st, y + 2, x + 1, qn);
-      dissipate<2>(val, half_inv, ly, qc, ys_w[ys_at(0, y + 2, x)], qn);
+      const double ju = qn[2];
+      dissipate<2>(val, half_inv, ly, qc, ys_r[ys_at(0, y + 2, x)], qn);
 #pragma unroll
       for (int u = 0; u < S; ++u) {   // x flux difference
-        const double fm = u == 0 ? qs<L>(st, y + 1, x, 1) : xs_w[xs_at(u, y, x)];
-        const double fc = u == 0 ? qc[1] : xs_w[xs_at(u, y, x + 1)];
-        const double fp = u == 0 ? qs<L>(st, y + 1, x + 2, 1) : xs_w[xs_at(u, y, x + 2)];
+        const double fm = u == 0 ? jl : xs_r[xs_at(u, y, x)];
+        const double fc = u == 0 ? qc[1] : xs_r[xs_at(u, y, x + 1)];
+        const double fp = u == 0 ? jr : xs_r[xs_at(u, y, x + 2)];
         val[u] = dadd(val[u], dmul(inv, dsub(dmul(0.5, dadd(fm, fc)), dmul(0.5, dadd(fc, fp)))));
       }
 #pragma unroll
       for (int u = 0; u < S; ++u) {   // y flux difference
-        const double fm = u == 0 ? qs<L>(st, y, x + 1, 2) : ys_w[ys_at(u, y, x)];
-        const double fc = u == 0 ? qc[2] : ys_w[ys_at(u, y + 1, x)];
-        const double fp = u == 0 ? qs<L>(st, y + 2, x + 1, 2) : ys_w[ys_at(u, y + 2, x)];
+        const double fm = u == 0 ? jd : ys_r[ys_at(u, y, x)];
+        const double fc = u == 0 ? qc[2] : ys_r[ys_at(u, y + 1, x)];
+        const double fp = u == 0 ? ju : ys_r[ys_at(u, y + 2, x)];
         val[u] = dadd(val[u], dmul(inv, dsub(dmul(0.5, dadd(fm, fc)), dmul(0.5, dadd(fc, fp)))));
       }
-      double* ob = outb + (g & 1) * OUTN;
+      double* ob = outb + (gp & 1) * OUTN;
 #pragma unroll
       for (int u = 0; u < S; ++u) {
         if (L == kAoS) ob[(y * P + x) * S + u] = val[u];
         else ob[u * P * P + y * P + x] = val[u];
       }
       fence_proxy_async();
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-        const unsigned long long v = __shfl_xor_sync(0xffffffffu, cmax, o);
-        cmax = v > cmax ? v : cmax;
-      }
-      if (lane == 0) wmax[(g & 1) * 8 + warp] = cmax;
+      // per-patch max wave speed: 64-bit max as (high word, then low word) warp reductions
+      const unsigned hi = (unsigned)(cmax >> 32), lo = (unsigned)cmax;
+      const unsigned mhi = __reduce_max_sync(0xffffffffu, hi);
+      const unsigned mlo = __reduce_max_sync(0xffffffffu, hi == mhi ? lo : 0u);
+      if (lane == 0) wmax[(gp & 1) * 8 + warp] = ((unsigned long long)mhi << 32) | mlo;
     }
-    pidx += gridDim.x;
-    stg = (stg + 1) & (NST - 1);
+    cmax = cnew;
+    if (producer) bulk_wait_read0();   // output buffer of patch g-1's parity is rewritten by B(g+1)
+    __syncthreads();
+    if (producer) {
+      if (g + NST - 1 < G) issue(g + NST - 1);   // into the stage of patch g-1, retired just now
+      if (g >= 1) {
+        store_out(g - 1);
+        finish_patch(g - 1);
+      }
+    }
+    stg = stg == NST - 1 ? 0 : stg + 1;
     par ^= (stg == 0);
     slot3 = slot3 == 2 ? 0 : slot3 + 1;
   }
 
   const int any_bad = __syncthreads_or(bad ? 1 : 0);
-  if (producer) {
-    if (G >= 1) {
-      store_out(G - 1);
-      finish_patch(G - 1);
-    }
-    bulk_wait_all0();
-  }
+  if (producer) bulk_wait_all0();
   if (tid == 0 && any_bad) atomicOr(status, 1u);
 }
 
