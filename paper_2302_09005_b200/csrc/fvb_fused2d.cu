@@ -153,6 +153,9 @@ fused2d_kernel(const double* __restrict__ qin, double* __restrict__ qout, const 
     const double inv = __ddiv_rn(dtv[pi], dx);
     invs[(g & 1) * 2] = inv;
     invs[(g & 1) * 2 + 1] = dmul(0.5, inv);   // `0.5 * inv * a` evaluates 0.5*inv first
+    // the flux rewrite needs 0.5*inv exact: 0 or |inv| >= 2^-1021, finite
+    const unsigned e = ((unsigned)__double2hiint(inv) >> 20) & 0x7ffu;
+    if (!(inv == 0.0 || (e >= 2u && e < 0x7ffu))) atomicOr(&slowflag[g % 3], 1u);
   };
   if (producer)
     for (int g = 0; g < NST - 1 && g < G; ++g) issue(g);
@@ -236,19 +239,22 @@ fused2d_kernel(const double* __restrict__ qin, double* __restrict__ qout, const 
       load_q<L>(st, y + 2, x + 1, qn);
       const double ju = qn[2];
       dissipate<2>(val, half_inv, ly, qc, ys_r[ys_at(0, y + 2, x)], qn);
+      // flux differences (vectorized.py:193-200) as RN(half_inv * RN(a - b)), a/b the
+      // unscaled face sums: bit-identical to RN(inv * RN(RN(0.5a) - RN(0.5b))) inside
+      // the range gate (no subnormals; see fvb_fused3d.cu add_flux).
 #pragma unroll
       for (int u = 0; u < S; ++u) {   // x flux difference
         const double fm = u == 0 ? jl : xs_r[xs_at(u, y, x)];
         const double fc = u == 0 ? qc[1] : xs_r[xs_at(u, y, x + 1)];
         const double fp = u == 0 ? jr : xs_r[xs_at(u, y, x + 2)];
-        val[u] = dadd(val[u], dmul(inv, dsub(dmul(0.5, dadd(fm, fc)), dmul(0.5, dadd(fc, fp)))));
+        val[u] = dadd(val[u], dmul(half_inv, dsub(dadd(fm, fc), dadd(fc, fp))));
       }
 #pragma unroll
       for (int u = 0; u < S; ++u) {   // y flux difference
         const double fm = u == 0 ? jd : ys_r[ys_at(u, y, x)];
         const double fc = u == 0 ? qc[2] : ys_r[ys_at(u, y + 1, x)];
         const double fp = u == 0 ? ju : ys_r[ys_at(u, y + 2, x)];
-        val[u] = dadd(val[u], dmul(inv, dsub(dmul(0.5, dadd(fm, fc)), dmul(0.5, dadd(fc, fp)))));
+        val[u] = dadd(val[u], dmul(half_inv, dsub(dadd(fm, fc), dadd(fc, fp))));
       }
       double* ob = outb + (gp & 1) * OUTN;
 #pragma unroll

@@ -86,17 +86,26 @@ __device__ __forceinline__ void put_xs(double* b, int y, int hx, const Side<3>& 
   for (int k = 0; k < 4; ++k) b[xs_at(k + 1, y, hx)] = s.f[k];
 }
 
-// vectorized.py:193-200 for one direction: inv*(0.5*(f_m+f_c) - 0.5*(f_c+f_p)),
-// component u of the three fluxes supplied by `fm/fc/fp(u)`.
+// vectorized.py:193-200 for one direction: RN(inv * RN(RN(0.5*a) - RN(0.5*b)))
+// with a = RN(f_m+f_c), b = RN(f_c+f_p), evaluated as RN(half_inv * RN(a - b)).
+// Scaling by 0.5 is exact and commutes with rounding whenever nothing is
+// subnormal: inside the range gate every flux is 0 or has magnitude >= 2^-601,
+// so a, b and a-b are 0 or >= 2^-705, and half_inv = 0.5*inv exactly (the
+// kernels route patches with 0 < |inv| < 2^-1021 to the exact redo path).
+// Hence the two forms are bit-identical there, at 2 DMUL less per term.
 template <class FM, class FC, class FP>
-__device__ __forceinline__ void add_flux(double (&val)[S], double inv, FM fm, FC fc, FP fp) {
+__device__ __forceinline__ void add_flux(double (&val)[S], double half_inv, FM fm, FC fc, FP fp) {
 #pragma unroll
   for (int u = 0; u < S; ++u) {
     const double c = fc(u);
-    const double favg_m = dmul(0.5, dadd(fm(u), c));
-    const double favg_p = dmul(0.5, dadd(c, fp(u)));
-    val[u] = dadd(val[u], dmul(inv, dsub(favg_m, favg_p)));
+    val[u] = dadd(val[u], dmul(half_inv, dsub(dadd(fm(u), c), dadd(c, fp(u)))));
   }
+}
+
+// 0 or |inv| >= 2^-1021 (0.5*inv exact), finite: the flux rewrite above applies.
+__device__ __forceinline__ bool inv_ok(double inv) {
+  const unsigned e = ((unsigned)__double2hiint(inv) >> 20) & 0x7ffu;
+  return inv == 0.0 || (e >= 2u && e < 0x7ffu);
 }
 
 __device__ __forceinline__ bool is_negzero(double v) {
@@ -190,7 +199,7 @@ fused3d_kernel(const double* __restrict__ qin, double* __restrict__ qout, const 
   // z-march carries: z-side data of the previous plane, and the previous z face
   // (its dissipation term seen from the lower cell, tp, and its flux average)
   Side<3> zprev;
-  double tp[S], favg_zm[S];
+  double tp[S], favg_zm[S];   // favg_zm: the unscaled sum f_{z-1} + f_z of the previous z face
   zprev.lam = 0.0;
 #pragma unroll
   for (int u = 0; u < S; ++u) { tp[u] = 0.0; favg_zm[u] = 0.0; }
@@ -206,6 +215,7 @@ fused3d_kernel(const double* __restrict__ qin, double* __restrict__ qout, const 
       const double dx = __ddiv_rn(cell_size[pidx * 3], (double)P);   // vectorized.py:169
       inv = __ddiv_rn(dtv[pidx], dx);                                  // vectorized.py:170
       half_inv = dmul(0.5, inv);                                       // `0.5 * inv * a`
+      if (interior && tid == 0 && !inv_ok(inv)) atomicOr(&slowflag[jp & 1], 1u);
     }
     const double* st = ring + stg * STAGE;
     mbar_wait(&bars[stg], par);
@@ -299,11 +309,11 @@ fused3d_kernel(const double* __restrict__ qin, double* __restrict__ qout, const 
           val[u] = dadd(val[u], tp[u]);
         }
         // flux differences x, y, z (vectorized.py:193-200)
-        add_flux(val, inv,
+        add_flux(val, half_inv,
                  [&](int u) { return u == 0 ? qs<L>(stc, y + 1, x, 1) : xs_r[xs_at(u, y, x)]; },
                  [&](int u) { return u == 0 ? qc[1] : xs_r[xs_at(u, y, x + 1)]; },
                  [&](int u) { return u == 0 ? qs<L>(stc, y + 1, x + 2, 1) : xs_r[xs_at(u, y, x + 2)]; });
-        add_flux(val, inv,
+        add_flux(val, half_inv,
                  [&](int u) { return u == 0 ? qs<L>(stc, y, x + 1, 2) : ys_r[ys_at(u, y, x)]; },
                  [&](int u) { return u == 0 ? qc[2] : ys_r[ys_at(u, y + 1, x)]; },
                  [&](int u) { return u == 0 ? qs<L>(stc, y + 2, x + 1, 2) : ys_r[ys_at(u, y + 2, x)]; });
@@ -311,9 +321,9 @@ fused3d_kernel(const double* __restrict__ qin, double* __restrict__ qout, const 
 #pragma unroll
         for (int u = 0; u < S; ++u) {
           const double c = u == 0 ? qc[3] : zprev.f[u - 1];
-          const double favg_p = dmul(0.5, dadd(c, u == 0 ? jz_up : zcur.f[u - 1]));
-          val[u] = dadd(val[u], dmul(inv, dsub(favg_zm[u], favg_p)));
-          favg_zm[u] = favg_p;
+          const double sum_p = dadd(c, u == 0 ? jz_up : zcur.f[u - 1]);
+          val[u] = dadd(val[u], dmul(half_inv, dsub(favg_zm[u], sum_p)));
+          favg_zm[u] = sum_p;
         }
         // fix_negzero: the re-used z- term can only differ from the reference's
         // in the sign of an exact zero, visible solely as a -0.0 result whose
@@ -345,7 +355,7 @@ fused3d_kernel(const double* __restrict__ qin, double* __restrict__ qout, const 
           const double qu = qs<L>(st, y + 1, x + 1, u);
           tp[u] = dmul(cz, dsub(qu, qc[u]));
           const double c = u == 0 ? qc[3] : zprev.f[u - 1];
-          favg_zm[u] = dmul(0.5, dadd(c, u == 0 ? qs<L>(st, y + 1, x + 1, 3) : zcur.f[u - 1]));
+          favg_zm[u] = dadd(c, u == 0 ? qs<L>(st, y + 1, x + 1, 3) : zcur.f[u - 1]);
         }
       }
     }
