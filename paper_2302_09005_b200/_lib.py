@@ -13,7 +13,8 @@ import os
 from .errors import ContractViolationError, DeviceError
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libfvb200.so")
+# FVB_LIB_PATH selects an alternative in-tree build (A/B measurements of kernel variants)
+LIB_PATH = os.environ.get("FVB_LIB_PATH") or os.path.join(HERE, "libfvb200.so")
 
 FVB_OK = 0
 FVB_ERR_CONTRACT = 1

@@ -46,7 +46,13 @@ using namespace f16;
 constexpr int P = 16, E = 18, S = 5;
 constexpr int PLANE = E * E;              // haloed volumes per plane
 constexpr int STAGE = PLANE * S;          // doubles per ring stage
-constexpr int NST = 3;   // planes g-1 and g are read in iteration g; g+1 is in flight
+#ifndef FVB3D_DIRECT_OUT
+#define FVB3D_DIRECT_OUT 0
+#endif
+// DIRECT_OUT: results go straight from registers to HBM (no staging); the
+// freed shared memory deepens the ring.
+constexpr bool DIRECT = FVB3D_DIRECT_OUT != 0;
+constexpr int NST = DIRECT ? 4 : 3;   // planes g-1 and g are read in iteration g; the rest in flight
 constexpr int NPL = E;                    // planes per patch
 constexpr int64_t VOL = (int64_t)E * E * E;
 constexpr int64_t IVOL = (int64_t)P * P * P;
@@ -56,7 +62,7 @@ constexpr int OFF_RING = 0;
 constexpr int OFF_YS = OFF_RING + NST * STAGE;
 constexpr int OFF_XS = OFF_YS + 2 * SIDE;
 constexpr int OFF_OUT = OFF_XS + 2 * SIDE;
-constexpr int OFF_WMAX = OFF_OUT + 2 * OUTN;   // output planes double-buffered
+constexpr int OFF_WMAX = OFF_OUT + (DIRECT ? 0 : 2 * OUTN);   // output planes double-buffered
 constexpr int OFF_FLAG = OFF_WMAX + 16;
 constexpr int OFF_BAR = OFF_FLAG + 1;
 constexpr int TOTAL = OFF_BAR + NST;
@@ -191,9 +197,10 @@ fused3d_kernel(const double* __restrict__ qin, double* __restrict__ qout, const 
   }
   __syncthreads();
   if (producer)
-    for (int g = 0; g < 2 && g < G; ++g) issue(g);
+    for (int g = 0; g < NST - 1 && g < G; ++g) issue(g);
 
   bool bad = false;
+  bool slow = false;           // some quotient of this thread's volumes left the range gate (this patch)
   unsigned long long cm = 0;   // running max wave speed (bit pattern) of this column
   double inv = 0.0, half_inv = 0.0;
   // z-march carries: z-side data of the previous plane, and the previous z face
@@ -215,7 +222,7 @@ fused3d_kernel(const double* __restrict__ qin, double* __restrict__ qout, const 
       const double dx = __ddiv_rn(cell_size[pidx * 3], (double)P);   // vectorized.py:169
       inv = __ddiv_rn(dtv[pidx], dx);                                  // vectorized.py:170
       half_inv = dmul(0.5, inv);                                       // `0.5 * inv * a`
-      if (interior && tid == 0 && !inv_ok(inv)) atomicOr(&slowflag[jp & 1], 1u);
+      if (tid == 0 && !inv_ok(inv)) slow = true;
     }
     const double* st = ring + stg * STAGE;
     mbar_wait(&bars[stg], par);
@@ -233,7 +240,7 @@ fused3d_kernel(const double* __restrict__ qin, double* __restrict__ qout, const 
         bool ok;
         const Thermo<3> T = closure_all_ranged<3>(q, cl, sd, ok);
         bad = bad || (ok && T.bad);
-        if (!ok) atomicOr(&slowflag[jp & 1], 1u);
+        slow = slow || !ok;
         unsigned long long m = (unsigned long long)__double_as_longlong(sd[0].lam);
         unsigned long long v = (unsigned long long)__double_as_longlong(sd[1].lam);
         m = v > m ? v : m;
@@ -247,7 +254,7 @@ fused3d_kernel(const double* __restrict__ qin, double* __restrict__ qout, const 
         bool ok;
         const Thermo<3> T = closure_one_ranged<3>(q, cl, 2, zcur, ok);
         bad = bad || (ok && T.bad);
-        if (!ok) atomicOr(&slowflag[jp & 1], 1u);
+        slow = slow || !ok;
       }
     } else if (full_plane) {
       {   // y-face halo rows (haloed y = 0, 17), interior columns
@@ -258,7 +265,7 @@ fused3d_kernel(const double* __restrict__ qin, double* __restrict__ qout, const 
         bool ok;
         const Thermo<3> T = closure_one_ranged<3>(q, cl, 1, sh, ok);
         bad = bad || (ok && T.bad);
-        if (!ok) atomicOr(&slowflag[jp & 1], 1u);
+        slow = slow || !ok;
         put_ys(ys_w, hy, x, sh);
       }
       {   // x-face halo columns (haloed x = 0, 17), interior rows
@@ -269,7 +276,7 @@ fused3d_kernel(const double* __restrict__ qin, double* __restrict__ qout, const 
         bool ok;
         const Thermo<3> T = closure_one_ranged<3>(q, cl, 0, sh, ok);
         bad = bad || (ok && T.bad);
-        if (!ok) atomicOr(&slowflag[jp & 1], 1u);
+        slow = slow || !ok;
         put_xs(xs_w, x, hx, sh);
       }
     }
@@ -341,13 +348,22 @@ fused3d_kernel(const double* __restrict__ qin, double* __restrict__ qout, const 
           }
         }
 #pragma unroll
-        double* ob = outb + (g & 1) * OUTN;
+        if (DIRECT) {
+          const int64_t cell = (int64_t)(zh - 2) * P * P + y * P + x;
 #pragma unroll
-        for (int u = 0; u < S; ++u) {
-          if (L == kAoS) ob[(y * P + x) * S + u] = val[u];
-          else ob[u * P * P + y * P + x] = val[u];
+          for (int u = 0; u < S; ++u) {
+            if (L == kAoS) __stcs(qout + (pidx * IVOL + cell) * S + u, val[u]);
+            else __stcs(qout + ((int64_t)u * n + pidx) * IVOL + cell, val[u]);
+          }
+        } else {
+          double* ob = outb + (g & 1) * OUTN;
+#pragma unroll
+          for (int u = 0; u < S; ++u) {
+            if (L == kAoS) ob[(y * P + x) * S + u] = val[u];
+            else ob[u * P * P + y * P + x] = val[u];
+          }
+          fence_proxy_async();
         }
-        fence_proxy_async();
       } else {
         // zh == 1: only the face (0 | 1) -- the minus face of the first interior plane
 #pragma unroll
@@ -358,6 +374,10 @@ fused3d_kernel(const double* __restrict__ qin, double* __restrict__ qout, const 
           favg_zm[u] = dadd(c, u == 0 ? qs<L>(st, y + 1, x + 1, 3) : zcur.f[u - 1]);
         }
       }
+    }
+    if (zh == NPL - 1) {   // patch complete: queue it for the exact path if any lane left the range gate
+      if (__any_sync(0xffffffffu, slow) && lane == 0) atomicOr(&slowflag[jp & 1], 1u);
+      slow = false;
     }
     if (interior) {
       zprev = zcur;
@@ -374,11 +394,11 @@ fused3d_kernel(const double* __restrict__ qin, double* __restrict__ qout, const 
     }
     // One barrier per plane: publishes this plane's side data and output, and
     // retires plane zh-1's stage and side buffers for reuse.
-    if (producer) bulk_wait_read0();   // output buffer (g+1)&1, written next iteration, is free
+    if (!DIRECT && producer) bulk_wait_read0();   // output buffer (g+1)&1, written next iteration, is free
     __syncthreads();
     if (producer) {
-      if (g + 2 < G) issue(g + 2);     // into the stage of plane g-1, retired just now
-      if (zh >= 2) store_out(g);
+      if (g + NST - 1 < G) issue(g + NST - 1);   // into the stage of plane g-1, retired just now
+      if (!DIRECT && zh >= 2) store_out(g);
       if (zh == NPL - 1) finish_patch_max(jp);
     }
     stg = stg == NST - 1 ? 0 : stg + 1;
