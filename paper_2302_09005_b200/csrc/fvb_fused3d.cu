@@ -230,42 +230,150 @@ fused3d_kernel(const double* __restrict__ qin, double* __restrict__ qout, const 
     double* ys_w = ysb + (g & 1) * SIDE;
     double* xs_w = xsb + (g & 1) * SIDE;
 
-    // ---------------- A: closures of plane zh ----------------
     Side<3> zcur;
-    if (interior) {
+    // ---------------- A: closures of plane zh (interior volume of this lane) ----------------
+    auto closure_full = [&]() {
       double q[S];
       load_q<L>(st, y + 1, x + 1, q);
-      if (full_plane) {
-        Side<3> sd[3];
-        bool ok;
-        const Thermo<3> T = closure_all_ranged<3>(q, cl, sd, ok);
-        bad = bad || (ok && T.bad);
-        slow = slow || !ok;
-        unsigned long long m = (unsigned long long)__double_as_longlong(sd[0].lam);
-        unsigned long long v = (unsigned long long)__double_as_longlong(sd[1].lam);
-        m = v > m ? v : m;
-        v = (unsigned long long)__double_as_longlong(sd[2].lam);
-        m = v > m ? v : m;
-        cm = m > cm ? m : cm;
-        put_xs(xs_w, y, x + 1, sd[0]);
-        put_ys(ys_w, y + 1, x, sd[1]);
-        zcur = sd[2];
+      Side<3> sd[3];
+      bool ok;
+      const Thermo<3> T = closure_all_ranged<3>(q, cl, sd, ok);
+      bad = bad | (ok & T.bad);
+      slow = slow | !ok;
+      unsigned long long m = (unsigned long long)__double_as_longlong(sd[0].lam);
+      unsigned long long v = (unsigned long long)__double_as_longlong(sd[1].lam);
+      m = v > m ? v : m;
+      v = (unsigned long long)__double_as_longlong(sd[2].lam);
+      m = v > m ? v : m;
+      cm = m > cm ? m : cm;
+      put_xs(xs_w, y, x + 1, sd[0]);
+      put_ys(ys_w, y + 1, x, sd[1]);
+      zcur = sd[2];
+    };
+    // ---------------- B: update of this lane's cell of plane zh-1 ----------------
+    // Reads plane zh-1's side data (published last iteration, behind the barrier
+    // that ended it) and this column's plane-zh z data (zcur): no barrier between
+    // A and B, and in the steady state both are one basic block the scheduler
+    // can interleave.
+    const double* stc = ring + (stg == 0 ? NST - 1 : stg - 1) * STAGE;   // plane zh-1
+    const double* ys_r = ysb + ((g - 1) & 1) * SIDE;
+    const double* xs_r = xsb + ((g - 1) & 1) * SIDE;
+    auto update_full = [&]() {
+      double qc[S], val[S], qn[S];
+      load_q<L>(stc, y + 1, x + 1, qc);
+      // z face (zh-1 | zh) seen from the lower cell: coeff*(Q_zh - Q_zh-1)
+      const double cz = dmul(half_inv, speed_max(zcur.lam, zprev.lam));
+#pragma unroll
+      for (int u = 0; u < S; ++u) val[u] = qc[u];                       // _pass_copy
+      // dissipation x-, x+, y-, y+ (vectorized.py:173-180)
+      const double lx = xs_r[xs_at(0, y, x + 1)];
+      load_q<L>(stc, y + 1, x, qn);
+      dissipate<3>(val, half_inv, lx, qc, xs_r[xs_at(0, y, x)], qn);
+      load_q<L>(stc, y + 1, x + 2, qn);
+      dissipate<3>(val, half_inv, lx, qc, xs_r[xs_at(0, y, x + 2)], qn);
+      const double ly = ys_r[ys_at(0, y + 1, x)];
+      load_q<L>(stc, y, x + 1, qn);
+      dissipate<3>(val, half_inv, ly, qc, ys_r[ys_at(0, y, x)], qn);
+      load_q<L>(stc, y + 2, x + 1, qn);
+      dissipate<3>(val, half_inv, ly, qc, ys_r[ys_at(0, y + 2, x)], qn);
+      // z-: the previous face's term, negated; z+: this face's term
+#pragma unroll
+      for (int u = 0; u < S; ++u) val[u] = dsub(val[u], tp[u]);
+#pragma unroll
+      for (int u = 0; u < S; ++u) {
+        tp[u] = dmul(cz, dsub(qs<L>(st, y + 1, x + 1, u), qc[u]));
+        val[u] = dadd(val[u], tp[u]);
+      }
+      // flux differences x, y, z (vectorized.py:193-200)
+      add_flux(val, half_inv,
+               [&](int u) { return u == 0 ? qs<L>(stc, y + 1, x, 1) : xs_r[xs_at(u, y, x)]; },
+               [&](int u) { return u == 0 ? qc[1] : xs_r[xs_at(u, y, x + 1)]; },
+               [&](int u) { return u == 0 ? qs<L>(stc, y + 1, x + 2, 1) : xs_r[xs_at(u, y, x + 2)]; });
+      add_flux(val, half_inv,
+               [&](int u) { return u == 0 ? qs<L>(stc, y, x + 1, 2) : ys_r[ys_at(u, y, x)]; },
+               [&](int u) { return u == 0 ? qc[2] : ys_r[ys_at(u, y + 1, x)]; },
+               [&](int u) { return u == 0 ? qs<L>(stc, y + 2, x + 1, 2) : ys_r[ys_at(u, y + 2, x)]; });
+      const double jz_up = qs<L>(st, y + 1, x + 1, 3);
+#pragma unroll
+      for (int u = 0; u < S; ++u) {
+        const double c = u == 0 ? qc[3] : zprev.f[u - 1];
+        const double sum_p = dadd(c, u == 0 ? jz_up : zcur.f[u - 1]);
+        val[u] = dadd(val[u], dmul(half_inv, dsub(favg_zm[u], sum_p)));
+        favg_zm[u] = sum_p;
+      }
+      // fix_negzero: the re-used z- term can only differ from the reference's
+      // in the sign of an exact zero, visible solely as a -0.0 result whose
+      // lower neighbour holds -0.0 in the same unknown (then the reference
+      // adds +0.0 and ends at +0.0).  Rare: check the input in HBM.
+      bool nz = false;
+#pragma unroll
+      for (int u = 0; u < S; ++u) nz = nz | is_negzero(val[u]);
+      if (__builtin_expect(nz, 0)) {
+        const int64_t vlow = ((int64_t)(zh - 2) * E + (y + 1)) * E + (x + 1);
+#pragma unroll
+        for (int u = 0; u < S; ++u) {
+          const double qlow = L == kAoS ? qin[(pidx * VOL + vlow) * S + u] : qin[((int64_t)u * n + pidx) * VOL + vlow];
+          if (is_negzero(val[u]) && is_negzero(qlow)) val[u] = 0.0;
+        }
+      }
+      if (DIRECT) {
+        const int64_t cell = (int64_t)(zh - 2) * P * P + y * P + x;
+#pragma unroll
+        for (int u = 0; u < S; ++u) {
+          if (L == kAoS) __stcs(qout + (pidx * IVOL + cell) * S + u, val[u]);
+          else __stcs(qout + ((int64_t)u * n + pidx) * IVOL + cell, val[u]);
+        }
       } else {
+        double* ob = outb + (g & 1) * OUTN;
+#pragma unroll
+        for (int u = 0; u < S; ++u) {
+          if (L == kAoS) ob[(y * P + x) * S + u] = val[u];
+          else ob[u * P * P + y * P + x] = val[u];
+        }
+        fence_proxy_async();
+      }
+    };
+
+    if (interior && zh >= 2 && zh <= P) {
+      // steady state: closures of plane zh and the update of plane zh-1, one block
+      closure_full();
+      update_full();
+    } else if (interior) {
+      if (full_plane) {
+        closure_full();
+      } else {   // z-halo planes: only their z-side data
+        double q[S];
+        load_q<L>(st, y + 1, x + 1, q);
         bool ok;
         const Thermo<3> T = closure_one_ranged<3>(q, cl, 2, zcur, ok);
-        bad = bad || (ok && T.bad);
-        slow = slow || !ok;
+        bad = bad | (ok & T.bad);
+        slow = slow | !ok;
+      }
+      if (zh == 1) {
+        // only the face (0 | 1) -- the minus face of the first interior plane
+        double qc[S];
+        load_q<L>(stc, y + 1, x + 1, qc);
+        const double cz = dmul(half_inv, speed_max(zcur.lam, zprev.lam));
+#pragma unroll
+        for (int u = 0; u < S; ++u) {
+          const double qu = qs<L>(st, y + 1, x + 1, u);
+          tp[u] = dmul(cz, dsub(qu, qc[u]));
+          const double c = u == 0 ? qc[3] : zprev.f[u - 1];
+          favg_zm[u] = dadd(c, u == 0 ? qs<L>(st, y + 1, x + 1, 3) : zcur.f[u - 1]);   // j_z of plane 1
+        }
+      } else if (zh == NPL - 1) {
+        update_full();
       }
     } else if (full_plane) {
-      {   // y-face halo rows (haloed y = 0, 17), interior columns
+      {   // halo warp: y-face halo rows (haloed y = 0, 17), interior columns
         const int hy = lane < 16 ? 0 : E - 1;
         double q[S];
         load_q<L>(st, hy, x + 1, q);
         Side<3> sh;
         bool ok;
         const Thermo<3> T = closure_one_ranged<3>(q, cl, 1, sh, ok);
-        bad = bad || (ok && T.bad);
-        slow = slow || !ok;
+        bad = bad | (ok & T.bad);
+        slow = slow | !ok;
         put_ys(ys_w, hy, x, sh);
       }
       {   // x-face halo columns (haloed x = 0, 17), interior rows
@@ -275,104 +383,9 @@ fused3d_kernel(const double* __restrict__ qin, double* __restrict__ qout, const 
         Side<3> sh;
         bool ok;
         const Thermo<3> T = closure_one_ranged<3>(q, cl, 0, sh, ok);
-        bad = bad || (ok && T.bad);
-        slow = slow || !ok;
+        bad = bad | (ok & T.bad);
+        slow = slow | !ok;
         put_xs(xs_w, x, hx, sh);
-      }
-    }
-    // No barrier here: the update below reads plane zh-1's side data (published
-    // last iteration, behind the barrier that ended it) and this column's own
-    // plane-zh z data.
-
-    // ---------------- B: update of the cells of plane zh-1 ----------------
-    if (interior && zh >= 1) {
-      const double* stc = ring + (stg == 0 ? NST - 1 : stg - 1) * STAGE;   // plane zh-1
-      const double* ys_r = ysb + ((g - 1) & 1) * SIDE;
-      const double* xs_r = xsb + ((g - 1) & 1) * SIDE;
-      double qc[S], val[S], qn[S];
-      load_q<L>(stc, y + 1, x + 1, qc);
-      // z face (zh-1 | zh) seen from the lower cell: coeff*(Q_zh - Q_zh-1)
-      const double cz = dmul(half_inv, speed_max(zcur.lam, zprev.lam));
-      if (zh >= 2) {
-#pragma unroll
-        for (int u = 0; u < S; ++u) val[u] = qc[u];                       // _pass_copy
-        // dissipation x-, x+, y-, y+ (vectorized.py:173-180)
-        const double lx = xs_r[xs_at(0, y, x + 1)];
-        load_q<L>(stc, y + 1, x, qn);
-        dissipate<3>(val, half_inv, lx, qc, xs_r[xs_at(0, y, x)], qn);
-        load_q<L>(stc, y + 1, x + 2, qn);
-        dissipate<3>(val, half_inv, lx, qc, xs_r[xs_at(0, y, x + 2)], qn);
-        const double ly = ys_r[ys_at(0, y + 1, x)];
-        load_q<L>(stc, y, x + 1, qn);
-        dissipate<3>(val, half_inv, ly, qc, ys_r[ys_at(0, y, x)], qn);
-        load_q<L>(stc, y + 2, x + 1, qn);
-        dissipate<3>(val, half_inv, ly, qc, ys_r[ys_at(0, y + 2, x)], qn);
-        // z-: the previous face's term, negated; z+: this face's term
-#pragma unroll
-        for (int u = 0; u < S; ++u) val[u] = dsub(val[u], tp[u]);
-#pragma unroll
-        for (int u = 0; u < S; ++u) {
-          tp[u] = dmul(cz, dsub(qs<L>(st, y + 1, x + 1, u), qc[u]));
-          val[u] = dadd(val[u], tp[u]);
-        }
-        // flux differences x, y, z (vectorized.py:193-200)
-        add_flux(val, half_inv,
-                 [&](int u) { return u == 0 ? qs<L>(stc, y + 1, x, 1) : xs_r[xs_at(u, y, x)]; },
-                 [&](int u) { return u == 0 ? qc[1] : xs_r[xs_at(u, y, x + 1)]; },
-                 [&](int u) { return u == 0 ? qs<L>(stc, y + 1, x + 2, 1) : xs_r[xs_at(u, y, x + 2)]; });
-        add_flux(val, half_inv,
-                 [&](int u) { return u == 0 ? qs<L>(stc, y, x + 1, 2) : ys_r[ys_at(u, y, x)]; },
-                 [&](int u) { return u == 0 ? qc[2] : ys_r[ys_at(u, y + 1, x)]; },
-                 [&](int u) { return u == 0 ? qs<L>(stc, y + 2, x + 1, 2) : ys_r[ys_at(u, y + 2, x)]; });
-        const double jz_up = qs<L>(st, y + 1, x + 1, 3);
-#pragma unroll
-        for (int u = 0; u < S; ++u) {
-          const double c = u == 0 ? qc[3] : zprev.f[u - 1];
-          const double sum_p = dadd(c, u == 0 ? jz_up : zcur.f[u - 1]);
-          val[u] = dadd(val[u], dmul(half_inv, dsub(favg_zm[u], sum_p)));
-          favg_zm[u] = sum_p;
-        }
-        // fix_negzero: the re-used z- term can only differ from the reference's
-        // in the sign of an exact zero, visible solely as a -0.0 result whose
-        // lower neighbour holds -0.0 in the same unknown (then the reference
-        // adds +0.0 and ends at +0.0).  Rare: check the input in HBM.
-        bool nz = false;
-#pragma unroll
-        for (int u = 0; u < S; ++u) nz = nz || is_negzero(val[u]);
-        if (__builtin_expect(nz, 0)) {
-          const int64_t vlow = ((int64_t)(zh - 2) * E + (y + 1)) * E + (x + 1);
-#pragma unroll
-          for (int u = 0; u < S; ++u) {
-            const double qlow = L == kAoS ? qin[(pidx * VOL + vlow) * S + u] : qin[((int64_t)u * n + pidx) * VOL + vlow];
-            if (is_negzero(val[u]) && is_negzero(qlow)) val[u] = 0.0;
-          }
-        }
-#pragma unroll
-        if (DIRECT) {
-          const int64_t cell = (int64_t)(zh - 2) * P * P + y * P + x;
-#pragma unroll
-          for (int u = 0; u < S; ++u) {
-            if (L == kAoS) __stcs(qout + (pidx * IVOL + cell) * S + u, val[u]);
-            else __stcs(qout + ((int64_t)u * n + pidx) * IVOL + cell, val[u]);
-          }
-        } else {
-          double* ob = outb + (g & 1) * OUTN;
-#pragma unroll
-          for (int u = 0; u < S; ++u) {
-            if (L == kAoS) ob[(y * P + x) * S + u] = val[u];
-            else ob[u * P * P + y * P + x] = val[u];
-          }
-          fence_proxy_async();
-        }
-      } else {
-        // zh == 1: only the face (0 | 1) -- the minus face of the first interior plane
-#pragma unroll
-        for (int u = 0; u < S; ++u) {
-          const double qu = qs<L>(st, y + 1, x + 1, u);
-          tp[u] = dmul(cz, dsub(qu, qc[u]));
-          const double c = u == 0 ? qc[3] : zprev.f[u - 1];
-          favg_zm[u] = dadd(c, u == 0 ? qs<L>(st, y + 1, x + 1, 3) : zcur.f[u - 1]);
-        }
       }
     }
     if (zh == NPL - 1) {   // patch complete: queue it for the exact path if any lane left the range gate
