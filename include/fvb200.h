@@ -128,6 +128,19 @@ int fvb_patch_max_eig(const fvb_spec* spec, const double* qin, double* max_eig, 
 int fvb_probe(int dim, double gamma, const double* states, int64_t n, double* lam, double* flux,
               double* pressure, uint8_t* bad, void* stream);
 
+/* Between steps: rebuild QIn (haloed) from QOut (interior) over a logical
+ * uniform patch grid, grid_shape[0..dim) = patch counts along x, y[, z]
+ * (patch index x-fastest), periodic wrap or zero-gradient edge.  Replaces
+ * mesh.halo_project (mesh.py:261-310) bit for bit, corners included. */
+int fvb_halo_project(const fvb_spec* spec, const double* qout, double* qin, const int32_t* grid_shape,
+                     int periodic, void* stream);
+
+/* Conserved totals: totals[u] = sum over all interior volumes of unknown u
+ * (deterministic order) -- the per-step diagnostics of run_simulation
+ * (SPEC.md:446-455, :473).  scratch: fvb_totals_scratch_bytes(spec) bytes. */
+size_t fvb_totals_scratch_bytes(const fvb_spec* spec);
+int fvb_totals(const fvb_spec* spec, const double* qout, double* scratch, double* totals, void* stream);
+
 /* Self-test: shared-reciprocal division vs IEEE division for n operand pairs. */
 int fvb_selftest_div(const double* a, const double* b, double* out_shared, double* out_ieee,
                      int64_t n, void* stream);

@@ -141,3 +141,30 @@ def synthetic_qin(dim: int, p: int, n: int, seed: int = 0, gamma: float = 1.4) -
     q[..., 1:1 + dim] = rho[..., None] * vel
     q[..., -1] = pr / (gamma - 1.0) + 0.5 * rho * np.sum(vel * vel, axis=-1)
     return q.reshape(n, v * (dim + 2))
+
+
+def halo_project(dim: int, p: int, qout: np.ndarray, grid, periodic: bool) -> np.ndarray:
+    """Restatement of mesh.halo_project (mesh.py:261-310) as index arithmetic (numpy):
+    haloed QIn of every patch from the grid's interior QOut, per-axis wrap / clamp."""
+    grid = tuple(int(g) for g in grid)
+    n = int(np.prod(grid))
+    s = dim + 2
+    e = p + 2
+    qo = np.asarray(qout).reshape(n, p ** dim, s)
+    qin = np.empty((n, e ** dim, s))
+    h = np.indices((e,) * dim).reshape(dim, -1)[::-1]           # rows: haloed x, y[, z]
+    for patch in range(n):
+        c, rem = [], patch
+        for a in range(dim):
+            rem, ca = divmod(rem, grid[a])
+            c.append(ca)
+        src_patch = np.zeros(h.shape[1], dtype=np.int64)
+        src_vol = np.zeros(h.shape[1], dtype=np.int64)
+        for a in reversed(range(dim)):
+            ext = grid[a] * p
+            gi = c[a] * p + h[a] - 1
+            gi = np.mod(gi, ext) if periodic else np.clip(gi, 0, ext - 1)
+            src_patch = src_patch * grid[a] + gi // p
+            src_vol = src_vol * p + gi % p
+        qin[patch] = qo[src_patch, src_vol]
+    return qin.reshape(n, -1)

@@ -30,6 +30,7 @@ EXPORTED = (
     "fvb_version", "fvb_strerror", "fvb_select_kernel", "fvb_update", "fvb_status_words",
     "fvb_update_host_workspace", "fvb_update_host", "fvb_locate", "fvb_pack", "fvb_unpack",
     "fvb_reduce_dt", "fvb_set_dt", "fvb_patch_max_eig", "fvb_probe", "fvb_selftest_div",
+    "fvb_halo_project", "fvb_totals_scratch_bytes", "fvb_totals",
 )
 
 
@@ -84,6 +85,12 @@ def load():
     L.fvb_patch_max_eig.argtypes = [sp, vp, vp, vp, vp]
     L.fvb_probe.restype = i32
     L.fvb_probe.argtypes = [i32, dbl, vp, i64, vp, vp, vp, vp, vp]
+    L.fvb_halo_project.restype = i32
+    L.fvb_halo_project.argtypes = [sp, vp, vp, vp, i32, vp]
+    L.fvb_totals_scratch_bytes.restype = ctypes.c_size_t
+    L.fvb_totals_scratch_bytes.argtypes = [sp]
+    L.fvb_totals.restype = i32
+    L.fvb_totals.argtypes = [sp, vp, vp, vp, vp]
     L.fvb_selftest_div.restype = i32
     L.fvb_selftest_div.argtypes = [vp, vp, vp, vp, i64, vp]
     _lib = L

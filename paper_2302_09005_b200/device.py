@@ -154,6 +154,29 @@ class DeviceBatch:
                                           _stream_handle(torch, stream)), "fvb_locate")
         return info.cpu().numpy().reshape(self.n_patches, nbox, 4)
 
+    def halo_project(self, grid_shape, periodic: bool = True, stream=None) -> None:
+        """QIn <- halo projection of QOut over the patch grid (mesh.py:261-310), on the device."""
+        from .mesh import check_grid
+
+        torch = _torch()
+        shape = check_grid(self.spec.dimensions, self.n_patches, grid_shape)
+        g = (ctypes.c_int32 * 3)(*(list(shape) + [1] * (3 - len(shape))))
+        _lib.check(_lib.load().fvb_halo_project(ctypes.byref(self.fvb_spec()), _vp(self.QOut), _vp(self.QIn), g,
+                                                int(bool(periodic)), _stream_handle(torch, stream)),
+                   "fvb_halo_project")
+
+    def totals(self, stream=None) -> np.ndarray:
+        """Per-unknown sums of QOut over all interior volumes (conservation diagnostics)."""
+        torch = _torch()
+        L = _lib.load()
+        fs = self.fvb_spec()
+        scratch = torch.empty(L.fvb_totals_scratch_bytes(ctypes.byref(fs)) // 8, dtype=torch.float64,
+                              device=self.device)
+        out = torch.empty(self.spec.unknowns, dtype=torch.float64, device=self.device)
+        _lib.check(L.fvb_totals(ctypes.byref(fs), _vp(self.QOut), _vp(scratch), _vp(out),
+                                _stream_handle(torch, stream)), "fvb_totals")
+        return out.cpu().numpy()
+
     def to_host(self, batch: PatchBatch) -> None:
         """Copy QOut (AoS) and max_eigenvalue back into a host PatchBatch."""
         batch.QOut.reshape(-1)[...] = self.qout_aos().cpu().numpy()
@@ -234,6 +257,21 @@ def locate_host(batch: PatchBatch, gamma: float, device=None, chunk_patches: int
                                     _stream_handle(torch, None)), "fvb_locate")
             out[p0:p1] = info.cpu().numpy().reshape(p1 - p0, nbox, 4)
     return out
+
+
+def halo_project_host(batch: PatchBatch, grid_shape, periodic: bool, device=None) -> None:
+    """mesh.halo_project on host arrays through the device kernel (AoS both ways)."""
+    torch = _torch()
+    dev = torch.device("cuda", torch.cuda.current_device() if device is None else device)
+    spec = batch.spec
+    with torch.cuda.device(dev):
+        qout = torch.from_numpy(np.ascontiguousarray(batch.QOut, dtype=np.float64).reshape(-1)).to(dev)
+        qin = torch.empty(batch.n_patches * spec.haloed_volumes * spec.unknowns, dtype=torch.float64, device=dev)
+        fs = _lib.spec(spec.dimensions, spec.volumes_per_axis, batch.n_patches, 1.4, 0)
+        g = (ctypes.c_int32 * 3)(*(list(grid_shape) + [1] * (3 - len(grid_shape))))
+        _lib.check(_lib.load().fvb_halo_project(ctypes.byref(fs), _vp(qout), _vp(qin), g, int(bool(periodic)),
+                                                _stream_handle(torch, None)), "fvb_halo_project")
+        batch.QIn.reshape(-1)[...] = qin.cpu().numpy()
 
 
 def probe(dim: int, gamma: float, states: np.ndarray):

@@ -90,3 +90,69 @@ def cfl_dt(db: DeviceBatch, cfl: float = 0.4, dx: float | None = None, group=Non
     s = CflStepper(db, cfl, dx, group)
     s.reduce_dt()
     return float(s.gmax.item()), float(s.dt_scalar.item())
+
+
+# --- multi-step driver ----------------------------------------------------
+
+CSV_HEADER = ("step", "t", "dt", "globalMaxEigenvalue", "totalMass", "totalMomentum", "totalEnergy")
+
+
+class SimulationResult:
+    """Per-step record of run_simulation: dt, global max wave speed and conserved totals."""
+
+    def __init__(self, dim: int):
+        self.dim = dim
+        self.t, self.dt, self.max_eigenvalue, self.totals = [], [], [], []
+
+    @property
+    def steps(self) -> int:
+        return len(self.dt)
+
+    def rows(self):
+        for k in range(len(self.totals)):
+            tot = self.totals[k]
+            yield (k, self.t[k], self.dt[k - 1] if k else 0.0, self.max_eigenvalue[k], float(tot[0]),
+                   " ".join(repr(float(v)) for v in tot[1:1 + self.dim]), float(tot[-1]))
+
+    def to_csv(self, path: str) -> None:
+        with open(path, "w") as f:
+            f.write(",".join(CSV_HEADER) + "\n")
+            for r in self.rows():
+                f.write(",".join(str(v) for v in r) + "\n")
+
+
+def run_simulation(db: DeviceBatch, grid_shape, steps: int, cfl: float = 0.4, periodic: bool = True,
+                   kernel="auto", dx: float | None = None) -> SimulationResult:
+    """Device-resident time loop on one GPU.
+
+    db.QOut holds the initial interior field of a logical uniform patch grid
+    (patch index x-fastest).  Per step: dt = (cfl*dx)/max wave speed of the
+    previous state (a pre-pass for the first step), the fused
+    update of every patch, and the halo projection that rebuilds QIn from the
+    new QOut (mesh.py:261-310).  Conserved totals are recorded per step.
+    """
+    import numpy as np
+
+    res = SimulationResult(db.spec.dimensions)
+    db.halo_project(grid_shape, periodic)
+    stepper = CflStepper(db, cfl=cfl, dx=dx, kernel=kernel)
+    stepper.prepass()
+    res.totals.append(db.totals())
+    res.t.append(0.0)
+    res.max_eigenvalue.append(float(stepper.gmax.item()))
+    t = 0.0
+    for _ in range(steps):
+        dt = float(stepper.dt_scalar.item())
+        db.update(kernel=kernel)
+        if db.nonphysical():
+            from .errors import NonPhysicalStateError
+            raise NonPhysicalStateError("non-physical state during run_simulation", step=len(res.dt))
+        stepper.reduce_dt()                       # next step's dt from this step's wave speeds
+        db.halo_project(grid_shape, periodic)
+        t += dt
+        res.dt.append(dt)
+        res.t.append(t)
+        res.max_eigenvalue.append(float(stepper.gmax.item()))
+        res.totals.append(db.totals())
+    res.totals = list(np.asarray(res.totals))
+    return res

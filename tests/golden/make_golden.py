@@ -256,6 +256,24 @@ def main():
                                         "gamma": 1.4, "expect": expect})
         print("error", name, expect[0])
 
+    # ---- halo_project cases (mesh.py:261-310) ---------------------------------------------------
+    manifest["halo_cases"] = []
+    halo_specs = [("halo_2d_p3_g2x3", 2, 3, (2, 3)), ("halo_2d_p4_g1x1", 2, 4, (1, 1)),
+                  ("halo_3d_p2_g2x2x3", 3, 2, (2, 2, 3)), ("halo_3d_p4_g1x2x1", 3, 4, (1, 2, 1))]
+    for name, d, p, grid in halo_specs:
+        n = int(np.prod(grid))
+        for periodic in (True, False):
+            rng = np.random.default_rng(300 + len(name) + periodic)
+            b = mesh.make_patch_batch(mesh.PatchSpec(d, p, d + 2), n)
+            b.QOut[...] = rng.standard_normal(b.QOut.shape)
+            b.QIn[...] = np.nan
+            mesh.halo_project(b, grid, periodic)
+            fname = f"{name}_{'per' if periodic else 'edge'}.fvb"
+            mesh.save_batch(b, os.path.join(HERE, fname))
+            manifest["halo_cases"].append({"name": fname[:-4], "file": fname, "dim": d, "p": p,
+                                           "grid": list(grid), "periodic": periodic})
+            print("halo", fname)
+
     with open(os.path.join(HERE, "manifest.json"), "w") as f:
         json.dump(manifest, f, indent=1)
 

@@ -1,0 +1,89 @@
+"""GPU tests of the between-step path: device halo_project (mesh.py:261-310) and the
+multi-step CFL driver -- conservation and constant-state properties."""
+
+import json
+import os
+
+import numpy as np
+import pytest
+
+import oracle
+from conftest import GOLDEN, assert_bits_equal, load_golden
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():  # pragma: no cover
+    pytest.skip("no CUDA device", allow_module_level=True)
+
+from paper_2302_09005_b200 import device, driver, mesh, pde  # noqa: E402
+from paper_2302_09005_b200.errors import ContractViolationError  # noqa: E402
+
+with open(os.path.join(GOLDEN, "manifest.json")) as _f:
+    HALO = json.load(_f)["halo_cases"]
+
+
+@pytest.mark.parametrize("case", HALO, ids=lambda c: c["name"])
+def test_halo_project_matches_reference(case):
+    gold = load_golden(case["file"])
+    b = gold.copy()
+    b.QIn[...] = np.nan
+    mesh.halo_project(b, case["grid"], case["periodic"])
+    assert_bits_equal(b.QIn, gold.QIn, case["name"])
+    db = device.DeviceBatch(gold.spec, gold.n_patches, 1.4, layout="soa")
+    db.pack_from(torch.from_numpy(gold.QOut.reshape(-1).copy()).cuda(), interior=True)
+    db.halo_project(case["grid"], case["periodic"])
+    out = torch.empty_like(db.QIn)
+    import ctypes
+    from paper_2302_09005_b200 import _lib
+    _lib.check(_lib.load().fvb_unpack(ctypes.byref(db.fvb_spec()), device._vp(db.QIn), device._vp(out), 0,
+                                      device._stream_handle(torch, None)), "unpack")
+    assert_bits_equal(out.cpu().numpy().reshape(gold.QIn.shape), gold.QIn, case["name"] + " soa")
+
+
+@pytest.mark.parametrize("dim,p,grid", [(3, 16, (4, 3, 2)), (2, 16, (8, 5)), (3, 4, (3, 3, 3))])
+def test_halo_project_random_vs_oracle(dim, p, grid):
+    n = int(np.prod(grid))
+    b = mesh.make_patch_batch(mesh.PatchSpec(dim, p, dim + 2), n)
+    b.QOut[...] = np.random.default_rng(n).standard_normal(b.QOut.shape)
+    for periodic in (True, False):
+        mesh.halo_project(b, grid, periodic)
+        assert_bits_equal(b.QIn, oracle.halo_project(dim, p, b.QOut, grid, periodic), f"{grid} {periodic}")
+    with pytest.raises(ContractViolationError):
+        mesh.halo_project(b, grid[:-1], True)
+
+
+def _db_with_field(dim, p, grid, qout):
+    n = int(np.prod(grid))
+    spec = mesh.PatchSpec(dim, p, dim + 2)
+    b = mesh.make_patch_batch(spec, n)
+    b.QOut[...] = qout
+    db = device.DeviceBatch(spec, n, 1.4)
+    db.QOut.copy_(torch.from_numpy(b.QOut.reshape(-1)))
+    return db
+
+
+def test_run_simulation_conserves_totals():
+    """on a periodic grid the conserved totals drift <= 1e-12 relative per 100 steps."""
+    dim, p, grid = 2, 16, (4, 4)
+    n = int(np.prod(grid))
+    q = oracle.synthetic_qin(dim, p, n, seed=4).reshape(n, (p + 2) ** dim, dim + 2)
+    interior = q.reshape(n, p + 2, p + 2, dim + 2)[:, 1:-1, 1:-1, :].reshape(n, -1)
+    db = _db_with_field(dim, p, grid, interior)
+    res = driver.run_simulation(db, grid, steps=100, cfl=0.4, periodic=True)
+    tot = np.asarray(res.totals)
+    scale = np.abs(tot[0]).max()
+    drift = np.abs(tot[-1] - tot[0]) / np.maximum(np.abs(tot[0]), scale * 1e-3)
+    assert res.steps == 100 and all(dt > 0 for dt in res.dt)
+    assert drift.max() <= 1e-12, drift
+
+
+def test_run_simulation_constant_state_is_fixed_point():
+    """SPEC.md run_simulation example: a constant state stays bitwise constant; dt stays constant."""
+    dim, p, grid = 3, 16, (2, 2, 2)
+    n = int(np.prod(grid))
+    state = pde.euler_state(1.2, [0.3, -0.1, 0.2], 0.8)
+    field = np.tile(state, (n, p ** dim))
+    db = _db_with_field(dim, p, grid, field)
+    res = driver.run_simulation(db, grid, steps=10, cfl=0.3, periodic=True)
+    assert_bits_equal(db.QOut.cpu().numpy().reshape(n, -1), field, "constant field after 10 steps")
+    assert len(set(res.dt)) == 1

@@ -59,3 +59,17 @@ def test_oracle_error_semantics_match_reference(case):
         msg = "non-positive density in pressure closure" if kind == 1 else \
             "negative pressure in eigenvalue evaluation"
         assert msg == exp["message"], exp
+
+
+def _halo_cases():
+    import json, os
+    from conftest import GOLDEN
+    with open(os.path.join(GOLDEN, "manifest.json")) as f:
+        return json.load(f).get("halo_cases", [])
+
+
+@pytest.mark.parametrize("case", _halo_cases(), ids=lambda c: c["name"])
+def test_oracle_halo_project_matches_reference(case):
+    b = load_golden(case["file"])
+    qin = oracle.halo_project(case["dim"], case["p"], b.QOut, case["grid"], case["periodic"])
+    assert_bits_equal(qin, b.QIn, case["name"])
