@@ -311,12 +311,14 @@ cudaError_t launch(const FvbArgs& a, cudaStream_t st) {
 }  // namespace fvb
 
 bool fvb_fused16_supported(int dim, int p, int layout) {
-  return p == 16 && (dim == 2 || dim == 3) && (layout == fvb::kAoS || layout == fvb::kSoA);
+  return (p == 16 && (dim == 2 || dim == 3) && (layout == fvb::kAoS || layout == fvb::kSoA)) ||
+         fvb_small3d_supported(dim, p, layout);
 }
 
 cudaError_t fvb_launch_fused16(const FvbArgs& a, cudaStream_t st) {
   using namespace fvb;
   if (a.n <= 0) return cudaSuccess;
+  if (a.p != 16) return fvb_launch_small3d(a, st);   // includes its redo pass
   cudaError_t e;
   if (a.dim == 3) e = fvb_launch_fused3d16(a, st);
   else e = a.layout == kAoS ? f2::launch<kAoS>(a, st) : f2::launch<kSoA>(a, st);

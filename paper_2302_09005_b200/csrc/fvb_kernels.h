@@ -25,6 +25,8 @@ cudaError_t fvb_launch_fused16(const FvbArgs& a, cudaStream_t st);
 cudaError_t fvb_launch_fused3d16(const FvbArgs& a, cudaStream_t st);
 cudaError_t fvb_launch_redo(const FvbArgs& a, cudaStream_t st);
 bool fvb_fused16_supported(int dim, int p, int layout);
+bool fvb_small3d_supported(int dim, int p, int layout);
+cudaError_t fvb_launch_small3d(const FvbArgs& a, cudaStream_t st);
 cudaError_t fvb_launch_locate(int dim, int p, int64_t n, double gamma, int layout, const double* qin,
                               BoxInfo* info, cudaStream_t st);
 cudaError_t fvb_launch_pack(const double* src, double* dst, int64_t n, int64_t vols, int s, int to_soa,

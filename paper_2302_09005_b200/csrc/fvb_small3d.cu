@@ -1,0 +1,290 @@
+// fvb_small3d.cu -- fused 3D Rusanov update for small patches (p = 4: BASELINE
+// config 4, 1M patches).
+//
+// A persistent CTA of 128 threads processes PPC = 2 patches per iteration
+// (one thread per interior cell).  The haloed patches of an iteration are
+// contiguous in HBM (AoS) and arrive with ONE TMA bulk copy into a 2-stage
+// ring.  Per iteration:
+//   A  every thread evaluates the closure of its interior volume (all three
+//      directions) and, in a second pass, the one-direction closures of the
+//      96 face-halo volumes of its patch are spread over the 64 threads;
+//      side data (lam, f[1..4]) goes to per-direction shared arrays. -- barrier
+//   B  every cell accumulates its six face terms from the side arrays in the
+//      reference order (vectorized.py:161-200) and writes the interior to a
+//      staging buffer stored with one TMA bulk store per iteration. -- barrier
+// Closures use the range-gated exact arithmetic of fvb_exact.cuh; patches
+// leaving the gate go to the exact redo list (fvb_redo_kernel).
+#include <cuda_runtime.h>
+
+#include "fvb_exact.cuh"
+#include "fvb_kernels.h"
+#include "fvb_layout.cuh"
+#include "fvb_tma.cuh"
+
+namespace fvb {
+namespace fs {
+
+using namespace f16;
+
+template <int P>
+struct Cfg {
+  static constexpr int S = 5;
+  static constexpr int E = P + 2;
+  static constexpr int VOL = E * E * E;             // haloed volumes per patch
+  static constexpr int IVOL = P * P * P;            // interior cells per patch
+  static constexpr int PPC = 128 / IVOL > 0 ? 128 / IVOL : 1;   // patches per CTA iteration
+  static constexpr int THREADS = PPC * IVOL;
+  static constexpr int NHALO = 6 * P * P;           // face-halo volumes per patch
+  static constexpr int LINE = E * P * P;            // records of one direction: (E along n) x P x P
+  static constexpr int STAGE = PPC * VOL * S;       // doubles per ring stage
+  static constexpr int NST = 2;
+  static constexpr int SIDE = 3 * S * LINE;         // side data of one patch, 3 directions
+  static constexpr int OUTN = PPC * IVOL * S;
+  static constexpr int OFF_RING = 0;
+  static constexpr int OFF_SIDE = OFF_RING + NST * STAGE;
+  static constexpr int OFF_OUT = OFF_SIDE + PPC * SIDE;
+  static constexpr int OFF_WMAX = OFF_OUT + OUTN;
+  static constexpr int OFF_FLAG = OFF_WMAX + PPC * (THREADS / 32);
+  static constexpr int OFF_BAR = OFF_FLAG + 1;
+  static constexpr int TOTAL = OFF_BAR + NST;
+  static constexpr size_t BYTES = (size_t)TOTAL * 8;
+};
+
+// record (direction n, component c) of the volume whose haloed coordinate along n
+// is hn and whose interior coordinates across n are (a, b): [n][c][b][a][hn]
+template <int P>
+__device__ __forceinline__ int side_at(int n, int c, int hn, int a, int b) {
+  using C = Cfg<P>;
+  return ((n * C::S + c) * P + b) * P * C::E + a * C::E + hn;
+}
+
+template <int P>
+__device__ __forceinline__ void put_rec(double* side, int n, int hn, int a, int b, const Side<3>& s) {
+  side[side_at<P>(n, 0, hn, a, b)] = s.lam;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) side[side_at<P>(n, k + 1, hn, a, b)] = s.f[k];
+}
+
+template <int P>
+__global__ void __launch_bounds__(Cfg<P>::THREADS)
+small3d_kernel(const double* __restrict__ qin, double* __restrict__ qout, const double* __restrict__ cell_size,
+               const double* __restrict__ dtv, double* __restrict__ max_eig, unsigned* __restrict__ status,
+               int64_t n_patches, Closure cl) {
+  using C = Cfg<P>;
+  constexpr int S = C::S, E = C::E;
+  extern __shared__ __align__(128) double sm[];
+  double* ring = sm + C::OFF_RING;
+  double* sideb = sm + C::OFF_SIDE;
+  double* outb = sm + C::OFF_OUT;
+  unsigned long long* wmax = reinterpret_cast<unsigned long long*>(sm + C::OFF_WMAX);
+  unsigned* slowflag = reinterpret_cast<unsigned*>(sm + C::OFF_FLAG);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sm + C::OFF_BAR);
+
+  const int tid = threadIdx.x;
+  const int lp = tid / C::IVOL;              // patch slot within the iteration
+  const int cell = tid % C::IVOL;
+  const int cx = cell % P, cy = (cell / P) % P, cz = cell / (P * P);
+  const int warp = tid >> 5, lane = tid & 31;
+  constexpr int WPP = C::IVOL >= 32 ? C::IVOL / 32 : 1;   // warps per patch
+  const int64_t ngroups = (n_patches + C::PPC - 1) / C::PPC;
+  const int G = ngroups > (int64_t)blockIdx.x ? (int)((ngroups - 1 - blockIdx.x) / gridDim.x + 1) : 0;
+  auto group_of = [&](int g) -> int64_t { return (int64_t)blockIdx.x + (int64_t)g * gridDim.x; };
+  auto patches_in = [&](int64_t grp) -> int {
+    const int64_t left = n_patches - grp * C::PPC;
+    return left < C::PPC ? (int)left : C::PPC;
+  };
+
+  auto issue = [&](int g) {
+    const int64_t grp = group_of(g);
+    const int np = patches_in(grp);
+    double* st = ring + (g % C::NST) * C::STAGE;
+    uint64_t* bar = bars + (g % C::NST);
+    fence_proxy_async();
+    mbar_expect_tx(bar, (uint32_t)(np * C::VOL * S * 8));
+    tma_load_1d(st, qin + grp * C::PPC * (int64_t)C::VOL * S, (uint32_t)(np * C::VOL * S * 8), bar);
+  };
+
+  if (tid == 0) {
+    for (int s = 0; s < C::NST; ++s) mbar_init(&bars[s], 1);
+    slowflag[0] = 0;
+    fence_mbar_init();
+  }
+  __syncthreads();
+  if (tid == 0)
+    for (int g = 0; g < C::NST && g < G; ++g) issue(g);
+
+  bool bad = false;
+  unsigned stg = 0, par = 0;
+  for (int g = 0; g < G; ++g) {
+    const int64_t grp = group_of(g);
+    const int np = patches_in(grp);
+    const bool active = lp < np;
+    const int64_t pidx = grp * C::PPC + lp;
+    const double* st = ring + stg * C::STAGE + lp * C::VOL * S;
+    double* side = sideb + lp * C::SIDE;
+    mbar_wait(&bars[stg], par);
+    auto qat = [&](int hx, int hy, int hz, int u) { return st[((hz * E + hy) * E + hx) * S + u]; };
+    auto load = [&](int hx, int hy, int hz, double (&q)[S]) {
+#pragma unroll
+      for (int u = 0; u < S; ++u) q[u] = qat(hx, hy, hz, u);
+    };
+
+    bool slow = false;
+    unsigned long long cmax = 0;
+    double inv = 0.0, half_inv = 0.0;
+    if (active) {
+      const double dx = __ddiv_rn(cell_size[pidx * 3], (double)P);   // vectorized.py:169
+      inv = __ddiv_rn(dtv[pidx], dx);                                  // vectorized.py:170
+      half_inv = dmul(0.5, inv);
+      const unsigned ie = ((unsigned)__double2hiint(inv) >> 20) & 0x7ffu;
+      slow = !(inv == 0.0 || (ie >= 2u && ie < 0x7ffu));
+      // ---- A1: closure of this thread's interior volume ----
+      double q[S];
+      load(cx + 1, cy + 1, cz + 1, q);
+      Side<3> sd[3];
+      bool ok;
+      const Thermo<3> T = closure_all_ranged<3>(q, cl, sd, ok);
+      bad = bad | (ok & T.bad);
+      slow = slow | !ok;
+      unsigned long long m = (unsigned long long)__double_as_longlong(sd[0].lam);
+      unsigned long long v = (unsigned long long)__double_as_longlong(sd[1].lam);
+      m = v > m ? v : m;
+      v = (unsigned long long)__double_as_longlong(sd[2].lam);
+      cmax = v > m ? v : m;
+      put_rec<P>(side, 0, cx + 1, cy, cz, sd[0]);
+      put_rec<P>(side, 1, cy + 1, cx, cz, sd[1]);
+      put_rec<P>(side, 2, cz + 1, cx, cy, sd[2]);
+      // ---- A2: face-halo volumes of this patch, one direction each ----
+      for (int h = cell; h < C::NHALO; h += C::IVOL) {
+        const int face = h / (P * P);          // 0: x-, 1: x+, 2: y-, 3: y+, 4: z-, 5: z+
+        const int a = h % P, b = (h / P) % P;  // interior coords across the face normal
+        const int nd = face >> 1;
+        const int hn = (face & 1) ? E - 1 : 0;
+        const int hx = nd == 0 ? hn : a + 1;
+        const int hy = nd == 1 ? hn : (nd == 0 ? a + 1 : b + 1);
+        const int hz = nd == 2 ? hn : b + 1;
+        double qh[S];
+        load(hx, hy, hz, qh);
+        Side<3> sh;
+        bool okh;
+        const Thermo<3> Th = closure_one_ranged<3>(qh, cl, nd, sh, okh);
+        bad = bad | (okh & Th.bad);
+        slow = slow | !okh;
+        put_rec<P>(side, nd, hn, a, b, sh);
+      }
+    }
+    if (__any_sync(0xffffffffu, slow) && lane == 0) atomicOr(slowflag, 1u << (lp & 31));
+    __syncthreads();
+
+    // ---- B: face terms and update of this thread's cell ----
+    if (active) {
+      double qc[S], qn[S], val[S];
+      load(cx + 1, cy + 1, cz + 1, qc);
+#pragma unroll
+      for (int u = 0; u < S; ++u) val[u] = qc[u];                       // _pass_copy
+      const int hcc[3] = {cx + 1, cy + 1, cz + 1};
+      const int ab[3][2] = {{cy, cz}, {cx, cz}, {cx, cy}};
+      // dissipation: x-, x+, y-, y+, z-, z+ (vectorized.py:173-180)
+#pragma unroll
+      for (int nd = 0; nd < 3; ++nd) {
+        const double lc = side[side_at<P>(nd, 0, hcc[nd], ab[nd][0], ab[nd][1])];
+#pragma unroll
+        for (int sh = -1; sh <= 1; sh += 2) {
+          int hq[3] = {hcc[0], hcc[1], hcc[2]};
+          hq[nd] += sh;
+          load(hq[0], hq[1], hq[2], qn);
+          dissipate<3>(val, half_inv, lc, qc, side[side_at<P>(nd, 0, hcc[nd] + sh, ab[nd][0], ab[nd][1])], qn);
+        }
+      }
+      // flux differences x, y, z (vectorized.py:193-200), exact half_inv form (fvb_fused3d.cu)
+#pragma unroll
+      for (int nd = 0; nd < 3; ++nd) {
+        int hm[3] = {hcc[0], hcc[1], hcc[2]}, hp[3] = {hcc[0], hcc[1], hcc[2]};
+        hm[nd] -= 1;
+        hp[nd] += 1;
+#pragma unroll
+        for (int u = 0; u < S; ++u) {
+          const double fm = u == 0 ? qat(hm[0], hm[1], hm[2], 1 + nd)
+                                   : side[side_at<P>(nd, u, hcc[nd] - 1, ab[nd][0], ab[nd][1])];
+          const double fc = u == 0 ? qc[1 + nd] : side[side_at<P>(nd, u, hcc[nd], ab[nd][0], ab[nd][1])];
+          const double fp = u == 0 ? qat(hp[0], hp[1], hp[2], 1 + nd)
+                                   : side[side_at<P>(nd, u, hcc[nd] + 1, ab[nd][0], ab[nd][1])];
+          val[u] = dadd(val[u], dmul(half_inv, dsub(dadd(fm, fc), dadd(fc, fp))));
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < S; ++u) outb[(lp * C::IVOL + cell) * S + u] = val[u];
+      fence_proxy_async();
+    }
+    // per-patch max wave speed: 64-bit max as (high word, low word) warp reductions
+    {
+      const unsigned hi = (unsigned)(cmax >> 32), lo = (unsigned)cmax;
+      const unsigned mhi = __reduce_max_sync(0xffffffffu, hi);
+      const unsigned mlo = __reduce_max_sync(0xffffffffu, hi == mhi ? lo : 0u);
+      if (lane == 0) wmax[warp] = ((unsigned long long)mhi << 32) | mlo;
+    }
+    __syncthreads();
+    if (tid == 0) {
+      // output of this group, per-patch maxima, redo list; then refill the freed stage
+      tma_store_1d(qout + grp * C::PPC * (int64_t)C::IVOL * S, outb, (uint32_t)(np * C::IVOL * S * 8));
+      bulk_commit();
+      const unsigned flags = slowflag[0];
+      for (int k = 0; k < np; ++k) {
+        unsigned long long m = 0;
+        for (int w = 0; w < WPP; ++w) {
+          const unsigned long long v = wmax[k * WPP + w];
+          m = v > m ? v : m;
+        }
+        max_eig[grp * C::PPC + k] = __longlong_as_double((long long)m);
+        if (flags & (1u << k)) {
+          const unsigned r = atomicAdd(&status[1], 1u);
+          status[2 + r] = (unsigned)(grp * C::PPC + k);
+        }
+      }
+      slowflag[0] = 0;
+      if (g + C::NST < G) issue(g + C::NST);   // stage of this group, fully consumed
+      bulk_wait_read0();                       // staging buffer reusable next iteration
+    }
+    __syncthreads();
+    stg = stg == C::NST - 1 ? 0 : stg + 1;
+    par ^= (stg == 0);
+  }
+  const int any_bad = __syncthreads_or(bad ? 1 : 0);
+  if (tid == 0) {
+    bulk_wait_all0();
+    if (any_bad) atomicOr(status, 1u);
+  }
+}
+
+template <int P>
+cudaError_t launch(const FvbArgs& a, cudaStream_t st) {
+  using C = Cfg<P>;
+  auto kfn = small3d_kernel<P>;
+  cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::BYTES);
+  if (e != cudaSuccess) return e;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  int per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kfn, C::THREADS, C::BYTES);
+  if (per_sm < 1) per_sm = 1;
+  const int64_t groups = (a.n + C::PPC - 1) / C::PPC;
+  int64_t grid = (int64_t)sms * per_sm;
+  if (grid > groups) grid = groups;
+  const Closure cl{a.gamma, a.gamma - 1.0};
+  kfn<<<(unsigned)grid, C::THREADS, C::BYTES, st>>>(a.qin, a.qout, a.cell_size, a.dt, a.max_eig, a.status, a.n,
+                                                    cl);
+  return cudaGetLastError();
+}
+
+}  // namespace fs
+}  // namespace fvb
+
+bool fvb_small3d_supported(int dim, int p, int layout) { return dim == 3 && p == 4 && layout == fvb::kAoS; }
+
+cudaError_t fvb_launch_small3d(const FvbArgs& a, cudaStream_t st) {
+  if (a.n <= 0) return cudaSuccess;
+  cudaError_t e = fvb::fs::launch<4>(a, st);
+  if (e != cudaSuccess) return e;
+  return fvb_launch_redo(a, st);
+}

@@ -44,7 +44,9 @@ def test_capi_contract_checks_without_gpu():
     ok = _lib.spec(3, 16, 0, 1.4)
     assert L.fvb_update(ctypes.byref(ok), None, None, None, None, None, None, 0, 1, None) == _lib.FVB_OK  # N == 0
     assert L.fvb_select_kernel(ctypes.byref(_lib.spec(3, 16, 5, 1.4))) == _lib.KERNEL_FUSED
-    assert L.fvb_select_kernel(ctypes.byref(_lib.spec(3, 4, 5, 1.4))) == _lib.KERNEL_GENERIC
+    assert L.fvb_select_kernel(ctypes.byref(_lib.spec(3, 4, 5, 1.4))) == _lib.KERNEL_FUSED
+    assert L.fvb_select_kernel(ctypes.byref(_lib.spec(3, 4, 5, 1.4, 1))) == _lib.KERNEL_GENERIC
+    assert L.fvb_select_kernel(ctypes.byref(_lib.spec(3, 5, 5, 1.4))) == _lib.KERNEL_GENERIC
     assert L.fvb_select_kernel(ctypes.byref(_lib.spec(2, 16, 5, 1.4, 1))) == _lib.KERNEL_FUSED
     assert L.fvb_update_host_workspace(ctypes.byref(_lib.spec(3, 16, 8, 1.4)), 4) > 4 * 233280 * 2
 
