@@ -43,9 +43,9 @@ struct Cfg {
   static constexpr int OFF_RING = 0;
   static constexpr int OFF_SIDE = OFF_RING + NST * STAGE;
   static constexpr int OFF_OUT = OFF_SIDE + PPC * SIDE;
-  static constexpr int OFF_WMAX = OFF_OUT + OUTN;
-  static constexpr int OFF_FLAG = OFF_WMAX + PPC * (THREADS / 32);
-  static constexpr int OFF_BAR = OFF_FLAG + 1;
+  static constexpr int OFF_WMAX = OFF_OUT + 2 * OUTN;   // output staging double-buffered
+  static constexpr int OFF_FLAG = OFF_WMAX + 2 * (THREADS / 32);   // wmax double-buffered
+  static constexpr int OFF_BAR = OFF_FLAG + 1;   // two 32-bit flag words
   static constexpr int TOTAL = OFF_BAR + NST;
   static constexpr size_t BYTES = (size_t)TOTAL * 8;
 };
@@ -106,7 +106,7 @@ small3d_kernel(const double* __restrict__ qin, double* __restrict__ qout, const 
 
   if (tid == 0) {
     for (int s = 0; s < C::NST; ++s) mbar_init(&bars[s], 1);
-    slowflag[0] = 0;
+    slowflag[0] = slowflag[1] = 0;
     fence_mbar_init();
   }
   __syncthreads();
@@ -167,13 +167,17 @@ small3d_kernel(const double* __restrict__ qin, double* __restrict__ qout, const 
         load(hx, hy, hz, qh);
         Side<3> sh;
         bool okh;
-        const Thermo<3> Th = closure_one_ranged<3>(qh, cl, nd, sh, okh);
+        Thermo<3> Th;
+        // nd is warp-uniform (a warp's 32 halo tasks lie on one face pair)
+        if (nd == 0) Th = closure_one_ranged<3>(qh, cl, 0, sh, okh);
+        else if (nd == 1) Th = closure_one_ranged<3>(qh, cl, 1, sh, okh);
+        else Th = closure_one_ranged<3>(qh, cl, 2, sh, okh);
         bad = bad | (okh & Th.bad);
         slow = slow | !okh;
         put_rec<P>(side, nd, hn, a, b, sh);
       }
     }
-    if (__any_sync(0xffffffffu, slow) && lane == 0) atomicOr(slowflag, 1u << (lp & 31));
+    if (__any_sync(0xffffffffu, slow) && lane == 0) atomicOr(&slowflag[g & 1], 1u << (lp & 31));
     __syncthreads();
 
     // ---- B: face terms and update of this thread's cell ----
@@ -213,7 +217,7 @@ small3d_kernel(const double* __restrict__ qin, double* __restrict__ qout, const 
         }
       }
 #pragma unroll
-      for (int u = 0; u < S; ++u) outb[(lp * C::IVOL + cell) * S + u] = val[u];
+      for (int u = 0; u < S; ++u) outb[(g & 1) * C::OUTN + (lp * C::IVOL + cell) * S + u] = val[u];
       fence_proxy_async();
     }
     // per-patch max wave speed: 64-bit max as (high word, low word) warp reductions
@@ -221,18 +225,20 @@ small3d_kernel(const double* __restrict__ qin, double* __restrict__ qout, const 
       const unsigned hi = (unsigned)(cmax >> 32), lo = (unsigned)cmax;
       const unsigned mhi = __reduce_max_sync(0xffffffffu, hi);
       const unsigned mlo = __reduce_max_sync(0xffffffffu, hi == mhi ? lo : 0u);
-      if (lane == 0) wmax[warp] = ((unsigned long long)mhi << 32) | mlo;
+      if (lane == 0) wmax[(g & 1) * (C::THREADS / 32) + warp] = ((unsigned long long)mhi << 32) | mlo;
     }
+    if (tid == 0) bulk_wait_read0();   // staging buffer (g & 1) was stored two iterations ago
     __syncthreads();
     if (tid == 0) {
       // output of this group, per-patch maxima, redo list; then refill the freed stage
-      tma_store_1d(qout + grp * C::PPC * (int64_t)C::IVOL * S, outb, (uint32_t)(np * C::IVOL * S * 8));
+      tma_store_1d(qout + grp * C::PPC * (int64_t)C::IVOL * S, outb + (g & 1) * C::OUTN,
+                   (uint32_t)(np * C::IVOL * S * 8));
       bulk_commit();
-      const unsigned flags = slowflag[0];
+      const unsigned flags = slowflag[g & 1];
       for (int k = 0; k < np; ++k) {
         unsigned long long m = 0;
         for (int w = 0; w < WPP; ++w) {
-          const unsigned long long v = wmax[k * WPP + w];
+          const unsigned long long v = wmax[(g & 1) * (C::THREADS / 32) + k * WPP + w];
           m = v > m ? v : m;
         }
         max_eig[grp * C::PPC + k] = __longlong_as_double((long long)m);
@@ -241,11 +247,9 @@ small3d_kernel(const double* __restrict__ qin, double* __restrict__ qout, const 
           status[2 + r] = (unsigned)(grp * C::PPC + k);
         }
       }
-      slowflag[0] = 0;
+      slowflag[g & 1] = 0;   // next set in iteration g+2, after the next barrier
       if (g + C::NST < G) issue(g + C::NST);   // stage of this group, fully consumed
-      bulk_wait_read0();                       // staging buffer reusable next iteration
     }
-    __syncthreads();
     stg = stg == C::NST - 1 ? 0 : stg + 1;
     par ^= (stg == 0);
   }
