@@ -168,75 +168,49 @@ fused2d_kernel(const double* __restrict__ qin, double* __restrict__ qout, const 
   // published in iteration g-1.  A(g) and B(g) touch different parities.
   for (int g = 0; g <= G; ++g) {
     const unsigned pstg = stg == 0 ? NST - 1 : stg - 1;   // stage of patch g-1
-    // ---------------- A: closures of patch g ----------------
+    const double* st = ring + stg * STAGE;
+    double* ys_w = ysb + (g & 1) * SIDE;
+    double* xs_w = xsb + (g & 1) * SIDE;
     unsigned long long cnew = 0;
-    if (g < G) {
-      const double* st = ring + stg * STAGE;
-      mbar_wait(&bars[stg], par);
-      double* ys_w = ysb + (g & 1) * SIDE;
-      double* xs_w = xsb + (g & 1) * SIDE;
-      if (interior) {
-        double q[S];
-        load_q<L>(st, y + 1, x + 1, q);
-        Side<2> sd[2];
-        bool ok;
-        const Thermo<2> T = closure_all_ranged<2>(q, cl, sd, ok);
-        bad = bad || (ok && T.bad);
-        if (!ok) atomicOr(&slowflag[slot3], 1u);
-        const unsigned long long a = (unsigned long long)__double_as_longlong(sd[0].lam);
-        const unsigned long long b = (unsigned long long)__double_as_longlong(sd[1].lam);
-        cnew = a > b ? a : b;
-        put_xs(xs_w, y, x + 1, sd[0]);
-        put_ys(ys_w, y + 1, x, sd[1]);
-      } else {
-        {   // y-face halo rows (haloed y = 0, 17)
-          const int hy = lane < 16 ? 0 : E - 1;
-          double q[S];
-          load_q<L>(st, hy, x + 1, q);
-          Side<2> sh;
-          bool ok;
-          const Thermo<2> T = closure_one_ranged<2>(q, cl, 1, sh, ok);
-          bad = bad || (ok && T.bad);
-          if (!ok) atomicOr(&slowflag[slot3], 1u);
-          put_ys(ys_w, hy, x, sh);
-        }
-        {   // x-face halo columns (haloed x = 0, 17)
-          const int hx = lane < 16 ? 0 : E - 1;
-          double q[S];
-          load_q<L>(st, x + 1, hx, q);
-          Side<2> sh;
-          bool ok;
-          const Thermo<2> T = closure_one_ranged<2>(q, cl, 0, sh, ok);
-          bad = bad || (ok && T.bad);
-          if (!ok) atomicOr(&slowflag[slot3], 1u);
-          put_xs(xs_w, x, hx, sh);
-        }
-        if (producer) put_inv(g);   // read by B(g+1), behind this iteration's barrier
-      }
-    }
-    // ---------------- B: update of patch g-1 ----------------
-    if (interior && g >= 1) {
-      const int gp = g - 1;
-      const double* st = ring + pstg * STAGE;
-      const double* ys_r = ysb + (gp & 1) * SIDE;
-      const double* xs_r = xsb + (gp & 1) * SIDE;
-      const double inv = invs[(gp & 1) * 2], half_inv = invs[(gp & 1) * 2 + 1];
+    bool slow = false;
+    // ---------------- A: closure of this lane's volume of patch g ----------------
+    auto closure_int = [&]() {
+      double q[S];
+      load_q<L>(st, y + 1, x + 1, q);
+      Side<2> sd[2];
+      bool ok;
+      const Thermo<2> T = closure_all_ranged<2>(q, cl, sd, ok);
+      bad = bad | (ok & T.bad);
+      slow = slow | !ok;
+      const unsigned long long a = (unsigned long long)__double_as_longlong(sd[0].lam);
+      const unsigned long long b = (unsigned long long)__double_as_longlong(sd[1].lam);
+      cnew = a > b ? a : b;
+      put_xs(xs_w, y, x + 1, sd[0]);
+      put_ys(ys_w, y + 1, x, sd[1]);
+    };
+    // ---------------- B: update of this lane's cell of patch g-1 ----------------
+    const int gp = g - 1;
+    const double* stp = ring + pstg * STAGE;
+    const double* ys_r = ysb + (gp & 1) * SIDE;
+    const double* xs_r = xsb + (gp & 1) * SIDE;
+    auto update_int = [&]() {
+      const double half_inv = invs[(gp & 1) * 2 + 1];
       double qc[S], qn[S], val[S];
-      load_q<L>(st, y + 1, x + 1, qc);
+      load_q<L>(stp, y + 1, x + 1, qc);
 #pragma unroll
       for (int u = 0; u < S; ++u) val[u] = qc[u];                       // _pass_copy
       const double lx = xs_r[xs_at(0, y, x + 1)];
-      load_q<L>(st, y + 1, x, qn);
+      load_q<L>(stp, y + 1, x, qn);
       const double jl = qn[1];
       dissipate<2>(val, half_inv, lx, qc, xs_r[xs_at(0, y, x)], qn);
-      load_q<L>(st, y + 1, x + 2, qn);
+      load_q<L>(stp, y + 1, x + 2, qn);
       const double jr = qn[1];
       dissipate<2>(val, half_inv, lx, qc, xs_r[xs_at(0, y, x + 2)], qn);
       const double ly = ys_r[ys_at(0, y + 1, x)];
-      load_q<L>(st, y, x + 1, qn);
+      load_q<L>(stp, y, x + 1, qn);
       const double jd = qn[2];
       dissipate<2>(val, half_inv, ly, qc, ys_r[ys_at(0, y, x)], qn);
-      load_q<L>(st, y + 2, x + 1, qn);
+      load_q<L>(stp, y + 2, x + 1, qn);
       const double ju = qn[2];
       dissipate<2>(val, half_inv, ly, qc, ys_r[ys_at(0, y + 2, x)], qn);
       // flux differences (vectorized.py:193-200) as RN(half_inv * RN(a - b)), a/b the
@@ -263,12 +237,52 @@ fused2d_kernel(const double* __restrict__ qin, double* __restrict__ qout, const 
         else ob[u * P * P + y * P + x] = val[u];
       }
       fence_proxy_async();
-      // per-patch max wave speed: 64-bit max as (high word, then low word) warp reductions
-      const unsigned hi = (unsigned)(cmax >> 32), lo = (unsigned)cmax;
-      const unsigned mhi = __reduce_max_sync(0xffffffffu, hi);
-      const unsigned mlo = __reduce_max_sync(0xffffffffu, hi == mhi ? lo : 0u);
-      if (lane == 0) wmax[(gp & 1) * 8 + warp] = ((unsigned long long)mhi << 32) | mlo;
+    };
+
+    if (interior) {
+      if (g < G) mbar_wait(&bars[stg], par);
+      if (g >= 1 && g < G) {   // steady state: one basic block the scheduler can interleave
+        closure_int();
+        update_int();
+      } else if (g < G) {
+        closure_int();
+      } else {
+        update_int();
+      }
+      if (g >= 1) {
+        // per-patch max wave speed: 64-bit max as (high word, then low word) warp reductions
+        const unsigned hi = (unsigned)(cmax >> 32), lo = (unsigned)cmax;
+        const unsigned mhi = __reduce_max_sync(0xffffffffu, hi);
+        const unsigned mlo = __reduce_max_sync(0xffffffffu, hi == mhi ? lo : 0u);
+        if (lane == 0) wmax[(gp & 1) * 8 + warp] = ((unsigned long long)mhi << 32) | mlo;
+      }
+    } else if (g < G) {
+      mbar_wait(&bars[stg], par);
+      {   // y-face halo rows (haloed y = 0, 17)
+        const int hy = lane < 16 ? 0 : E - 1;
+        double q[S];
+        load_q<L>(st, hy, x + 1, q);
+        Side<2> sh;
+        bool ok;
+        const Thermo<2> T = closure_one_ranged<2>(q, cl, 1, sh, ok);
+        bad = bad | (ok & T.bad);
+        slow = slow | !ok;
+        put_ys(ys_w, hy, x, sh);
+      }
+      {   // x-face halo columns (haloed x = 0, 17)
+        const int hx = lane < 16 ? 0 : E - 1;
+        double q[S];
+        load_q<L>(st, x + 1, hx, q);
+        Side<2> sh;
+        bool ok;
+        const Thermo<2> T = closure_one_ranged<2>(q, cl, 0, sh, ok);
+        bad = bad | (ok & T.bad);
+        slow = slow | !ok;
+        put_xs(xs_w, x, hx, sh);
+      }
+      if (producer) put_inv(g);   // read by B(g+1), behind this iteration's barrier
     }
+    if (__any_sync(0xffffffffu, slow) && lane == 0) atomicOr(&slowflag[slot3], 1u);
     cmax = cnew;
     if (producer) bulk_wait_read0();   // output buffer of patch g-1's parity is rewritten by B(g+1)
     __syncthreads();
