@@ -54,9 +54,27 @@ def launches(path):
     return agg
 
 
+def inst_mix(rep, cells):
+    out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass"],
+                         capture_output=True, text=True).stdout
+    rows = list(csv.reader(io.StringIO(out)))
+    if len(rows) < 3:
+        return None
+    hdr, data = rows[1], rows[2:]
+    isrc, iex = hdr.index("Source"), hdr.index("Instructions Executed")
+    import re
+    agg = collections.Counter()
+    for r in data:
+        m = re.match(r"(@!?U?P\w+\s+)?([A-Z0-9_]+)", r[isrc].strip())
+        if m:
+            agg[m.group(2)] += float(r[iex] or 0)
+    return {k: v * 32 / cells for k, v in agg.items()}
+
+
 def main():
     tag, rep, lcsv = sys.argv[1:4]
     alg = float(sys.argv[4]) if len(sys.argv) > 4 else None
+    cells = float(sys.argv[5]) if len(sys.argv) > 5 else None
     os.makedirs(os.path.join("profiles", tag), exist_ok=True)
     m = raw_metrics(rep)
     lines = [f"# ncu summary `{tag}`", "", f"source: `{os.path.basename(rep)}` (ncu --set full, --clock-control none), "
@@ -75,6 +93,15 @@ def main():
     lines += ["", "## Warp stall reasons (cycles per issued instruction)", "", "| reason | value |", "|---|---|"]
     for v, k in stalls(m)[:12]:
         lines.append(f"| {k} | {v:.3f} |")
+    if cells:
+        mix = inst_mix(rep, cells)
+        if mix:
+            tot = sum(mix.values())
+            fp64 = sum(v for k, v in mix.items() if k in ("DADD", "DMUL", "DFMA", "DSETP"))
+            lines += ["", f"## Instruction mix (thread instructions per cell update; {cells:.0f} cells per launch)", "",
+                      f"total {tot:.1f}, FP64 {fp64:.1f}", "", "| opcode | per cell |", "|---|---|"]
+            for k, v in sorted(mix.items(), key=lambda t: -t[1])[:20]:
+                lines.append(f"| {k} | {v:.1f} |")
     agg = launches(lcsv)
     tot = sum(sum(v) for v in agg.values())
     lines += ["", "## Launch list (cold-cache, serialised; compare shares)", "",
