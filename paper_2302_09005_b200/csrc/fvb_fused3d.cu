@@ -46,6 +46,18 @@ using namespace f16;
 constexpr int P = 16, E = 18, S = 5;
 constexpr int PLANE = E * E;              // haloed volumes per plane
 constexpr int STAGE = PLANE * S;          // doubles per ring stage
+#ifndef FVB3D_TMEM
+#define FVB3D_TMEM 0
+#endif
+// TMEM (off by default): each interior thread parks its own volume's state and
+// x/y side data (15 doubles) in its tensor-memory lane row between the closure
+// (iteration g) and the update (iteration g+1) instead of re-reading them from
+// shared memory.  Measured on B200: bit-exact, but 23.4 vs 34.0 Gcell/s -- the
+// tcgen05.ld/wait::ld round trips stall the warps more than the shared-memory
+// loads they replace, so the scratchpad stays in shared memory.
+constexpr bool USE_TMEM = FVB3D_TMEM != 0;
+constexpr uint32_t TMEM_COLS = 128;   // 2 warps per lane quadrant x 2 plane parities x 32 columns
+
 #ifndef FVB3D_DIRECT_OUT
 #define FVB3D_DIRECT_OUT 0
 #endif
@@ -64,7 +76,8 @@ constexpr int OFF_XS = OFF_YS + 2 * SIDE;
 constexpr int OFF_OUT = OFF_XS + 2 * SIDE;
 constexpr int OFF_WMAX = OFF_OUT + (DIRECT ? 0 : 2 * OUTN);   // output planes double-buffered
 constexpr int OFF_FLAG = OFF_WMAX + 16;
-constexpr int OFF_BAR = OFF_FLAG + 1;
+constexpr int OFF_TMEM = OFF_FLAG + 1;   // TMEM base address (4 B) + padding
+constexpr int OFF_BAR = OFF_TMEM + 1;
 constexpr int TOTAL = OFF_BAR + NST;
 constexpr size_t BYTES = (size_t)TOTAL * 8;
 
@@ -131,6 +144,7 @@ fused3d_kernel(const double* __restrict__ qin, double* __restrict__ qout, const 
   unsigned long long* wmax = reinterpret_cast<unsigned long long*>(sm + OFF_WMAX);
   unsigned* slowflag = reinterpret_cast<unsigned*>(sm + OFF_FLAG);   // 2 words, by patch parity
   uint64_t* bars = reinterpret_cast<uint64_t*>(sm + OFF_BAR);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sm + OFF_TMEM);
 
   const int tid = threadIdx.x;
   const bool interior = tid < 256;
@@ -195,7 +209,13 @@ fused3d_kernel(const double* __restrict__ qin, double* __restrict__ qout, const 
     slowflag[0] = slowflag[1] = 0;
     fence_mbar_init();
   }
+  if (USE_TMEM && warp == 0) tmem_alloc(tmem_slot, TMEM_COLS);
+  if (USE_TMEM) tmem_fence_before();
   __syncthreads();
+  if (USE_TMEM) tmem_fence_after();
+  // this thread's TMEM row: lane quadrant of its warp, 64 columns per warp pair member
+  const uint32_t tm_base = USE_TMEM ? *tmem_slot + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)(64 * ((warp >> 2) & 1))
+                                    : 0u;
   if (producer)
     for (int g = 0; g < NST - 1 && g < G; ++g) issue(g);
 
@@ -249,6 +269,12 @@ fused3d_kernel(const double* __restrict__ qin, double* __restrict__ qout, const 
       put_xs(xs_w, y, x + 1, sd[0]);
       put_ys(ys_w, y + 1, x, sd[1]);
       zcur = sd[2];
+      if (USE_TMEM) {   // own state and x/y side data for the update of this plane next iteration
+        const uint32_t ta = tm_base + 32u * (uint32_t)(g & 1);
+        tmem_st5(ta, q);
+        tmem_st5(ta + 10, &sd[0].lam);
+        tmem_st5(ta + 20, &sd[1].lam);
+      }
     };
     // ---------------- B: update of this lane's cell of plane zh-1 ----------------
     // Reads plane zh-1's side data (published last iteration, behind the barrier
@@ -260,18 +286,27 @@ fused3d_kernel(const double* __restrict__ qin, double* __restrict__ qout, const 
     const double* xs_r = xsb + ((g - 1) & 1) * SIDE;
     auto update_full = [&]() {
       double qc[S], val[S], qn[S];
-      load_q<L>(stc, y + 1, x + 1, qc);
+      const uint32_t ta = tm_base + 32u * (uint32_t)((g - 1) & 1);   // TMEM record of plane zh-1
+      double lx, ly;
+      if (USE_TMEM) {
+        tmem_wait_st();
+        tmem_ld5(ta, qc);
+        lx = tmem_ld1(ta + 10);
+        ly = tmem_ld1(ta + 20);
+      } else {
+        load_q<L>(stc, y + 1, x + 1, qc);
+        lx = xs_r[xs_at(0, y, x + 1)];
+        ly = ys_r[ys_at(0, y + 1, x)];
+      }
       // z face (zh-1 | zh) seen from the lower cell: coeff*(Q_zh - Q_zh-1)
       const double cz = dmul(half_inv, speed_max(zcur.lam, zprev.lam));
 #pragma unroll
       for (int u = 0; u < S; ++u) val[u] = qc[u];                       // _pass_copy
       // dissipation x-, x+, y-, y+ (vectorized.py:173-180)
-      const double lx = xs_r[xs_at(0, y, x + 1)];
       load_q<L>(stc, y + 1, x, qn);
       dissipate<3>(val, half_inv, lx, qc, xs_r[xs_at(0, y, x)], qn);
       load_q<L>(stc, y + 1, x + 2, qn);
       dissipate<3>(val, half_inv, lx, qc, xs_r[xs_at(0, y, x + 2)], qn);
-      const double ly = ys_r[ys_at(0, y + 1, x)];
       load_q<L>(stc, y, x + 1, qn);
       dissipate<3>(val, half_inv, ly, qc, ys_r[ys_at(0, y, x)], qn);
       load_q<L>(stc, y + 2, x + 1, qn);
@@ -285,14 +320,28 @@ fused3d_kernel(const double* __restrict__ qin, double* __restrict__ qout, const 
         val[u] = dadd(val[u], tp[u]);
       }
       // flux differences x, y, z (vectorized.py:193-200)
-      add_flux(val, half_inv,
-               [&](int u) { return u == 0 ? qs<L>(stc, y + 1, x, 1) : xs_r[xs_at(u, y, x)]; },
-               [&](int u) { return u == 0 ? qc[1] : xs_r[xs_at(u, y, x + 1)]; },
-               [&](int u) { return u == 0 ? qs<L>(stc, y + 1, x + 2, 1) : xs_r[xs_at(u, y, x + 2)]; });
-      add_flux(val, half_inv,
-               [&](int u) { return u == 0 ? qs<L>(stc, y, x + 1, 2) : ys_r[ys_at(u, y, x)]; },
-               [&](int u) { return u == 0 ? qc[2] : ys_r[ys_at(u, y + 1, x)]; },
-               [&](int u) { return u == 0 ? qs<L>(stc, y + 2, x + 1, 2) : ys_r[ys_at(u, y + 2, x)]; });
+      {
+        double fo[4];
+        if (USE_TMEM) tmem_ld4(ta + 12, fo);
+        else
+#pragma unroll
+          for (int k = 0; k < 4; ++k) fo[k] = xs_r[xs_at(k + 1, y, x + 1)];
+        add_flux(val, half_inv,
+                 [&](int u) { return u == 0 ? qs<L>(stc, y + 1, x, 1) : xs_r[xs_at(u, y, x)]; },
+                 [&](int u) { return u == 0 ? qc[1] : fo[u - 1]; },
+                 [&](int u) { return u == 0 ? qs<L>(stc, y + 1, x + 2, 1) : xs_r[xs_at(u, y, x + 2)]; });
+      }
+      {
+        double fo[4];
+        if (USE_TMEM) tmem_ld4(ta + 22, fo);
+        else
+#pragma unroll
+          for (int k = 0; k < 4; ++k) fo[k] = ys_r[ys_at(k + 1, y + 1, x)];
+        add_flux(val, half_inv,
+                 [&](int u) { return u == 0 ? qs<L>(stc, y, x + 1, 2) : ys_r[ys_at(u, y, x)]; },
+                 [&](int u) { return u == 0 ? qc[2] : fo[u - 1]; },
+                 [&](int u) { return u == 0 ? qs<L>(stc, y + 2, x + 1, 2) : ys_r[ys_at(u, y + 2, x)]; });
+      }
       const double jz_up = qs<L>(st, y + 1, x + 1, 3);
 #pragma unroll
       for (int u = 0; u < S; ++u) {
@@ -423,7 +472,12 @@ fused3d_kernel(const double* __restrict__ qin, double* __restrict__ qout, const 
     }
   }
 
+  if (USE_TMEM) tmem_fence_before();
   const int any_bad = __syncthreads_or(bad ? 1 : 0);
+  if (USE_TMEM) {
+    tmem_fence_after();
+    if (warp == 0) tmem_dealloc(*tmem_slot, TMEM_COLS);
+  }
   if (producer) bulk_wait_all0();
   if (tid == 0 && any_bad) atomicOr(status, 1u);
 }
