@@ -110,14 +110,21 @@ int fvb_update(const fvb_spec* spec, const double* qin, double* qout, const doub
 }
 
 static size_t status_bytes(int64_t chunk) { return ((size_t)(chunk + 2) * 4 + 255) / 256 * 256; }
+static size_t align256(size_t b) { return (b + 255) / 256 * 256; }
+// One buffer set of the host pipeline: qin, qout, cell_size, dt, max_eig, each
+// 256-byte aligned (the fused kernels move patches with TMA bulk copies, which
+// need 16-byte aligned global addresses whatever the chunk length).
+static size_t host_set_bytes(const fvb_spec* spec, int64_t chunk) {
+  const fvb::Geom g = fvb::make_geom(spec->dim, spec->p, chunk);
+  return align256((size_t)chunk * g.V * g.s * 8) + align256((size_t)chunk * g.I * g.s * 8) +
+         align256((size_t)chunk * spec->dim * 8) + 2 * align256((size_t)chunk * 8);
+}
 
 size_t fvb_status_words(int64_t n_patches) { return (size_t)(n_patches + 2); }
 
 size_t fvb_update_host_workspace(const fvb_spec* spec, int64_t chunk) {
   if (check_spec(spec) || chunk < 1) return 0;
-  const fvb::Geom g = fvb::make_geom(spec->dim, spec->p, chunk);
-  const size_t per = (size_t)chunk * (g.V * g.s + g.I * g.s + spec->dim + 2) * sizeof(double);
-  return 2 * per + 2 * status_bytes(chunk);
+  return 2 * host_set_bytes(spec, chunk) + 2 * status_bytes(chunk);
 }
 
 int fvb_update_host(const fvb_spec* spec, const double* qin_h, double* qout_h, const double* cell_size_h,
@@ -137,16 +144,16 @@ int fvb_update_host(const fvb_spec* spec, const double* qin_h, double* qout_h, c
   // two status buffers (flag, redo count, redo list), one per buffer set
   uint32_t* status_b[2] = {reinterpret_cast<uint32_t*>(base),
                            reinterpret_cast<uint32_t*>(base + status_bytes(chunk))};
-  double* bufs = reinterpret_cast<double*>(base + 2 * status_bytes(chunk));
-  const size_t per = (size_t)chunk * (g.V * s + g.I * s + d + 2);
+  char* bufs = base + 2 * status_bytes(chunk);
+  const size_t per = host_set_bytes(spec, chunk);
   double *qin_d[2], *qout_d[2], *cs_d[2], *dt_d[2], *me_d[2];
   for (int b = 0; b < 2; ++b) {
-    double* p = bufs + b * per;
-    qin_d[b] = p; p += (size_t)chunk * g.V * s;
-    qout_d[b] = p; p += (size_t)chunk * g.I * s;
-    cs_d[b] = p; p += (size_t)chunk * d;
-    dt_d[b] = p; p += chunk;
-    me_d[b] = p;
+    char* p = bufs + b * per;
+    qin_d[b] = reinterpret_cast<double*>(p); p += align256((size_t)chunk * g.V * s * 8);
+    qout_d[b] = reinterpret_cast<double*>(p); p += align256((size_t)chunk * g.I * s * 8);
+    cs_d[b] = reinterpret_cast<double*>(p); p += align256((size_t)chunk * d * 8);
+    dt_d[b] = reinterpret_cast<double*>(p); p += align256((size_t)chunk * 8);
+    me_d[b] = reinterpret_cast<double*>(p);
   }
   cudaStream_t comp = as_stream(stream);
   cudaStream_t h2d = nullptr, d2h = nullptr;

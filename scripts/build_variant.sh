@@ -1,0 +1,20 @@
+#!/bin/bash
+# Build an A/B variant of libfvb200.so with extra nvcc flags (here, CPU cross-compile):
+#   scripts/build_variant.sh NAME [-DFOO=1 ...]  ->  paper_2302_09005_b200/_variants/libfvb200_NAME.so
+# Select it at run time with FVB_LIB_PATH=<that path>.
+set -e
+NAME=$1; shift
+ROOT=$(cd "$(dirname "$0")/.." && pwd)
+SRC=$ROOT/paper_2302_09005_b200/csrc
+OUT=$ROOT/paper_2302_09005_b200/_variants
+B=$(mktemp -d)
+mkdir -p "$OUT"
+FLAGS="-gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 -fmad=false -Xcompiler -fPIC $*"
+for f in fvb_capi fvb_generic fvb_fused2d fvb_fused3d fvb_small3d; do
+  /usr/local/cuda/bin/nvcc $FLAGS -Xptxas -v -c "$SRC/$f.cu" -o "$B/$f.o" 2> "$B/$f.log" &
+done
+wait
+grep -h -A2 "fused3d_kernelILi0ELi2" "$B/fvb_fused3d.log" | grep -E "registers|spill" || true
+/usr/local/cuda/bin/nvcc -gencode arch=compute_100a,code=sm_100a -shared -o "$OUT/libfvb200_$NAME.so" "$B"/*.o
+rm -rf "$B"
+echo "$OUT/libfvb200_$NAME.so"
