@@ -71,7 +71,7 @@ int fvb_select_kernel(const fvb_spec* spec);
  *   cell_size  [N*dim]  only cell_size[patch*dim + 0] is read (vectorized.py:169)
  *   dt         [N]      per-patch time step, must be >= 0 (checked by the host)
  *   max_eig    [N]      per-patch max directional wave speed (written, vectorized.py:226-231)
- *   status     [N+2]    device words (fvb_status_words): status[0] is ORed with 1 when a
+ *   status     [2N+2]   device words (fvb_status_words): status[0] is ORed with 1 when a
  *                       face-box volume has rho <= 0 or p < 0; status[1] / status[2..] are
  *                       the redo list the fused kernels use for patches whose quotients need
  *                       CUDA's division slow path (re-evaluated exactly before returning).
@@ -81,7 +81,9 @@ int fvb_update(const fvb_spec* spec, const double* qin, double* qout, const doub
                const double* dt, double* max_eig, uint32_t* status, int kernel, int zero_status,
                void* stream);
 
-/* Number of uint32 status words fvb_update needs for n patches (n + 2). */
+/* Number of uint32 status words fvb_update needs for n patches (2n + 2: the
+ * 3D p=16 kernel evaluates each patch as two halves, and each half may queue
+ * its patch on the redo list). */
 size_t fvb_status_words(int64_t n_patches);
 
 /* Same step from HOST arrays (the reference's calling convention, numpy

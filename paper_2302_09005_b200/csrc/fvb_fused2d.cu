@@ -20,6 +20,8 @@
 // list in the status buffer and re-evaluated exactly by fvb_redo_kernel.
 #include <cuda_runtime.h>
 
+#include <cstdlib>
+
 #include "fvb_exact.cuh"
 #include "fvb_kernels.h"
 #include "fvb_layout.cuh"
@@ -329,12 +331,23 @@ bool fvb_fused16_supported(int dim, int p, int layout) {
          fvb_small3d_supported(dim, p, layout);
 }
 
+// 3D p=16 kernel choice: half-patch CTAs (default) or full-patch CTAs
+// (FVB_3D_KERNEL=full, kept for A/B measurements).
+bool fvb_fused3d_use_half() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("FVB_3D_KERNEL");
+    v = (e && e[0] == 'f') ? 0 : 1;
+  }
+  return v == 1;
+}
+
 cudaError_t fvb_launch_fused16(const FvbArgs& a, cudaStream_t st) {
   using namespace fvb;
   if (a.n <= 0) return cudaSuccess;
   if (a.p != 16) return fvb_launch_small3d(a, st);   // includes its redo pass
   cudaError_t e;
-  if (a.dim == 3) e = fvb_launch_fused3d16(a, st);
+  if (a.dim == 3) e = fvb_fused3d_use_half() ? fvb_launch_fused3d16_half(a, st) : fvb_launch_fused3d16(a, st);
   else e = a.layout == kAoS ? f2::launch<kAoS>(a, st) : f2::launch<kSoA>(a, st);
   if (e != cudaSuccess) return e;
   return fvb_launch_redo(a, st);   // exact re-evaluation of queued patches (usually none)

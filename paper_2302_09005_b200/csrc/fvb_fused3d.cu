@@ -32,6 +32,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdlib>
+#include <type_traits>
 
 #include "fvb_exact.cuh"
 #include "fvb_kernels.h"
@@ -46,25 +47,7 @@ using namespace f16;
 constexpr int P = 16, E = 18, S = 5;
 constexpr int PLANE = E * E;              // haloed volumes per plane
 constexpr int STAGE = PLANE * S;          // doubles per ring stage
-#ifndef FVB3D_TMEM
-#define FVB3D_TMEM 0
-#endif
-// TMEM (off by default): each interior thread parks its own volume's state and
-// x/y side data (15 doubles) in its tensor-memory lane row between the closure
-// (iteration g) and the update (iteration g+1) instead of re-reading them from
-// shared memory.  Measured on B200: bit-exact, but 23.4 vs 34.0 Gcell/s -- the
-// tcgen05.ld/wait::ld round trips stall the warps more than the shared-memory
-// loads they replace, so the scratchpad stays in shared memory.
-constexpr bool USE_TMEM = FVB3D_TMEM != 0;
-constexpr uint32_t TMEM_COLS = 128;   // 2 warps per lane quadrant x 2 plane parities x 32 columns
-
-#ifndef FVB3D_DIRECT_OUT
-#define FVB3D_DIRECT_OUT 0
-#endif
-// DIRECT_OUT: results go straight from registers to HBM (no staging); the
-// freed shared memory deepens the ring.
-constexpr bool DIRECT = FVB3D_DIRECT_OUT != 0;
-constexpr int NST = DIRECT ? 4 : 3;   // planes g-1 and g are read in iteration g; the rest in flight
+constexpr int NST = 3;                    // ring stages: planes g-1 and g are read in iteration g, g+1 in flight
 constexpr int NPL = E;                    // planes per patch
 constexpr int64_t VOL = (int64_t)E * E * E;
 constexpr int64_t IVOL = (int64_t)P * P * P;
@@ -74,11 +57,11 @@ constexpr int OFF_RING = 0;
 constexpr int OFF_YS = OFF_RING + NST * STAGE;
 constexpr int OFF_XS = OFF_YS + 2 * SIDE;
 constexpr int OFF_OUT = OFF_XS + 2 * SIDE;
-constexpr int OFF_WMAX = OFF_OUT + (DIRECT ? 0 : 2 * OUTN);   // output planes double-buffered
+constexpr int OFF_WMAX = OFF_OUT + 2 * OUTN;   // output planes double-buffered
 constexpr int OFF_FLAG = OFF_WMAX + 16;
-constexpr int OFF_TMEM = OFF_FLAG + 1;   // TMEM base address (4 B) + padding
-constexpr int OFF_BAR = OFF_TMEM + 1;
+constexpr int OFF_BAR = OFF_FLAG + 1;
 constexpr int TOTAL = OFF_BAR + NST;
+constexpr int NTHREADS = 288;             // 8 interior warps (one column each) + the halo / producer warp
 constexpr size_t BYTES = (size_t)TOTAL * 8;
 
 template <int L>
@@ -131,8 +114,13 @@ __device__ __forceinline__ bool is_negzero(double v) {
   return (unsigned long long)__double_as_longlong(v) == 0x8000000000000000ull;
 }
 
+// Plane kinds of the z march (haloed plane index zh = 0 .. 17).
+enum PlaneKind { kZLo = 0, kFirst = 1, kSteady = 2, kZHi = 3 };
+template <int K>
+using Kind = std::integral_constant<int, K>;
+
 template <int L, int MINB>
-__global__ void __launch_bounds__(288, MINB)
+__global__ void __launch_bounds__(NTHREADS, MINB)
 fused3d_kernel(const double* __restrict__ qin, double* __restrict__ qout, const double* __restrict__ cell_size,
                const double* __restrict__ dtv, double* __restrict__ max_eig, unsigned* __restrict__ status,
                int64_t n, Closure cl) {
@@ -144,24 +132,22 @@ fused3d_kernel(const double* __restrict__ qin, double* __restrict__ qout, const 
   unsigned long long* wmax = reinterpret_cast<unsigned long long*>(sm + OFF_WMAX);
   unsigned* slowflag = reinterpret_cast<unsigned*>(sm + OFF_FLAG);   // 2 words, by patch parity
   uint64_t* bars = reinterpret_cast<uint64_t*>(sm + OFF_BAR);
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sm + OFF_TMEM);
 
   const int tid = threadIdx.x;
   const bool interior = tid < 256;
   const int warp = tid >> 5, lane = tid & 31;
   const int x = lane & 15;
   const int y = ((warp & 7) << 1) | (lane >> 4);
-  const bool producer = tid == 256;
+  const bool producer = tid == 256;   // TMA issue / output store / patch max
 
   const int my_patches = (n > (int64_t)blockIdx.x) ? (int)((n - 1 - (int64_t)blockIdx.x) / gridDim.x + 1) : 0;
-  const int G = my_patches * NPL;   // planes this CTA streams (iteration count)
-  auto patch_of = [&](int g) -> int64_t { return (int64_t)blockIdx.x + (int64_t)(g / NPL) * gridDim.x; };
+  auto patch_index = [&](int j) -> int64_t { return (int64_t)blockIdx.x + (int64_t)j * gridDim.x; };
 
-  auto issue = [&](int g) {
-    const int64_t pidx = patch_of(g);
-    const int zh = g % NPL;
-    double* st = ring + (g % NST) * STAGE;
-    uint64_t* bar = bars + (g % NST);
+  // plane zh of this CTA's j-th patch into ring stage s
+  auto issue = [&](int j, int zh, unsigned s) {
+    const int64_t pidx = patch_index(j);
+    double* st = ring + s * STAGE;
+    uint64_t* bar = bars + s;
     fence_proxy_async();
     mbar_expect_tx(bar, (uint32_t)(STAGE * 8));
     if (L == kAoS) {
@@ -173,10 +159,8 @@ fused3d_kernel(const double* __restrict__ qin, double* __restrict__ qout, const 
                     (uint32_t)(PLANE * 8), bar);
     }
   };
-  auto store_out = [&](int g) {   // output of iteration g: interior plane zh-2, buffer g & 1
-    const int64_t pidx = patch_of(g);
-    const int z = g % NPL - 2;
-    const double* src = outb + (g & 1) * OUTN;
+  auto store_out = [&](int64_t pidx, int z) {   // interior plane z from output buffer z & 1
+    const double* src = outb + (z & 1) * OUTN;
     if (L == kAoS) {
       tma_store_1d(qout + (pidx * IVOL + (int64_t)z * P * P) * S, src, (uint32_t)(OUTN * 8));
     } else {
@@ -187,14 +171,13 @@ fused3d_kernel(const double* __restrict__ qin, double* __restrict__ qout, const 
     }
     bulk_commit();
   };
-  auto finish_patch_max = [&](int j) {
+  auto finish_patch_max = [&](int j, int64_t pidx) {
     unsigned long long m = wmax[(j & 1) * 8];
 #pragma unroll
     for (int w = 1; w < 8; ++w) {
       const unsigned long long v = wmax[(j & 1) * 8 + w];
       m = v > m ? v : m;
     }
-    const int64_t pidx = (int64_t)blockIdx.x + (int64_t)j * gridDim.x;
     max_eig[pidx] = __longlong_as_double((long long)m);
     if (slowflag[j & 1]) {   // queue the patch for the exact re-evaluation (fvb_redo_kernel)
       const unsigned k = atomicAdd(&status[1], 1u);
@@ -209,275 +192,230 @@ fused3d_kernel(const double* __restrict__ qin, double* __restrict__ qout, const 
     slowflag[0] = slowflag[1] = 0;
     fence_mbar_init();
   }
-  if (USE_TMEM && warp == 0) tmem_alloc(tmem_slot, TMEM_COLS);
-  if (USE_TMEM) tmem_fence_before();
   __syncthreads();
-  if (USE_TMEM) tmem_fence_after();
-  // this thread's TMEM row: lane quadrant of its warp, 64 columns per warp pair member
-  const uint32_t tm_base = USE_TMEM ? *tmem_slot + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)(64 * ((warp >> 2) & 1))
-                                    : 0u;
-  if (producer)
-    for (int g = 0; g < NST - 1 && g < G; ++g) issue(g);
+  if (producer && my_patches > 0) {
+    issue(0, 0, 0);
+    issue(0, 1, 1);
+  }
 
   bool bad = false;
   bool slow = false;           // some quotient of this thread's volumes left the range gate (this patch)
   unsigned long long cm = 0;   // running max wave speed (bit pattern) of this column
-  double inv = 0.0, half_inv = 0.0;
   // z-march carries: z-side data of the previous plane, and the previous z face
-  // (its dissipation term seen from the lower cell, tp, and its flux average)
+  // (its dissipation term seen from the lower cell, tp, and the unscaled flux
+  // sum f_{z-1} + f_z, favg_zm)
   Side<3> zprev;
-  double tp[S], favg_zm[S];   // favg_zm: the unscaled sum f_{z-1} + f_z of the previous z face
+  double tp[S], favg_zm[S];
   zprev.lam = 0.0;
 #pragma unroll
   for (int u = 0; u < S; ++u) { tp[u] = 0.0; favg_zm[u] = 0.0; }
 #pragma unroll
   for (int k = 0; k < 4; ++k) zprev.f[k] = 0.0;
 
-  // per-iteration indices advanced incrementally (no 64-bit div/mod in the loop)
-  int zh = 0, jp = 0;                  // plane within the patch, patch ordinal of this CTA
-  int64_t pidx = blockIdx.x;           // patch index
-  unsigned stg = 0, par = 0;           // ring stage of plane g and its mbarrier parity
-  for (int g = 0; g < G; ++g) {
-    if (zh == 0) {
-      const double dx = __ddiv_rn(cell_size[pidx * 3], (double)P);   // vectorized.py:169
-      inv = __ddiv_rn(dtv[pidx], dx);                                  // vectorized.py:170
-      half_inv = dmul(0.5, inv);                                       // `0.5 * inv * a`
-      if (tid == 0 && !inv_ok(inv)) slow = true;
-    }
-    const double* st = ring + stg * STAGE;
-    mbar_wait(&bars[stg], par);
-    const bool full_plane = zh >= 1 && zh <= P;
-    double* ys_w = ysb + (g & 1) * SIDE;
-    double* xs_w = xsb + (g & 1) * SIDE;
+  unsigned stg = 0, par = 0;   // ring stage of the current plane and its mbarrier phase parity
 
-    Side<3> zcur;
-    // ---------------- A: closures of plane zh (interior volume of this lane) ----------------
-    auto closure_full = [&]() {
-      double q[S];
-      load_q<L>(st, y + 1, x + 1, q);
-      Side<3> sd[3];
-      bool ok;
-      const Thermo<3> T = closure_all_ranged<3>(q, cl, sd, ok);
-      bad = bad | (ok & T.bad);
-      slow = slow | !ok;
-      unsigned long long m = (unsigned long long)__double_as_longlong(sd[0].lam);
-      unsigned long long v = (unsigned long long)__double_as_longlong(sd[1].lam);
-      m = v > m ? v : m;
-      v = (unsigned long long)__double_as_longlong(sd[2].lam);
-      m = v > m ? v : m;
-      cm = m > cm ? m : cm;
-      put_xs(xs_w, y, x + 1, sd[0]);
-      put_ys(ys_w, y + 1, x, sd[1]);
-      zcur = sd[2];
-      if (USE_TMEM) {   // own state and x/y side data for the update of this plane next iteration
-        const uint32_t ta = tm_base + 32u * (uint32_t)(g & 1);
-        tmem_st5(ta, q);
-        tmem_st5(ta + 10, &sd[0].lam);
-        tmem_st5(ta + 20, &sd[1].lam);
-      }
-    };
-    // ---------------- B: update of this lane's cell of plane zh-1 ----------------
-    // Reads plane zh-1's side data (published last iteration, behind the barrier
-    // that ended it) and this column's plane-zh z data (zcur): no barrier between
-    // A and B, and in the steady state both are one basic block the scheduler
-    // can interleave.
-    const double* stc = ring + (stg == 0 ? NST - 1 : stg - 1) * STAGE;   // plane zh-1
-    const double* ys_r = ysb + ((g - 1) & 1) * SIDE;
-    const double* xs_r = xsb + ((g - 1) & 1) * SIDE;
-    auto update_full = [&]() {
-      double qc[S], val[S], qn[S];
-      const uint32_t ta = tm_base + 32u * (uint32_t)((g - 1) & 1);   // TMEM record of plane zh-1
-      double lx, ly;
-      if (USE_TMEM) {
-        tmem_wait_st();
-        tmem_ld5(ta, qc);
-        lx = tmem_ld1(ta + 10);
-        ly = tmem_ld1(ta + 20);
-      } else {
-        load_q<L>(stc, y + 1, x + 1, qc);
-        lx = xs_r[xs_at(0, y, x + 1)];
-        ly = ys_r[ys_at(0, y + 1, x)];
-      }
-      // z face (zh-1 | zh) seen from the lower cell: coeff*(Q_zh - Q_zh-1)
-      const double cz = dmul(half_inv, speed_max(zcur.lam, zprev.lam));
-#pragma unroll
-      for (int u = 0; u < S; ++u) val[u] = qc[u];                       // _pass_copy
-      // dissipation x-, x+, y-, y+ (vectorized.py:173-180)
-      load_q<L>(stc, y + 1, x, qn);
-      dissipate<3>(val, half_inv, lx, qc, xs_r[xs_at(0, y, x)], qn);
-      load_q<L>(stc, y + 1, x + 2, qn);
-      dissipate<3>(val, half_inv, lx, qc, xs_r[xs_at(0, y, x + 2)], qn);
-      load_q<L>(stc, y, x + 1, qn);
-      dissipate<3>(val, half_inv, ly, qc, ys_r[ys_at(0, y, x)], qn);
-      load_q<L>(stc, y + 2, x + 1, qn);
-      dissipate<3>(val, half_inv, ly, qc, ys_r[ys_at(0, y + 2, x)], qn);
-      // z-: the previous face's term, negated; z+: this face's term
-#pragma unroll
-      for (int u = 0; u < S; ++u) val[u] = dsub(val[u], tp[u]);
-#pragma unroll
-      for (int u = 0; u < S; ++u) {
-        tp[u] = dmul(cz, dsub(qs<L>(st, y + 1, x + 1, u), qc[u]));
-        val[u] = dadd(val[u], tp[u]);
-      }
-      // flux differences x, y, z (vectorized.py:193-200)
-      {
-        double fo[4];
-        if (USE_TMEM) tmem_ld4(ta + 12, fo);
-        else
-#pragma unroll
-          for (int k = 0; k < 4; ++k) fo[k] = xs_r[xs_at(k + 1, y, x + 1)];
-        add_flux(val, half_inv,
-                 [&](int u) { return u == 0 ? qs<L>(stc, y + 1, x, 1) : xs_r[xs_at(u, y, x)]; },
-                 [&](int u) { return u == 0 ? qc[1] : fo[u - 1]; },
-                 [&](int u) { return u == 0 ? qs<L>(stc, y + 1, x + 2, 1) : xs_r[xs_at(u, y, x + 2)]; });
-      }
-      {
-        double fo[4];
-        if (USE_TMEM) tmem_ld4(ta + 22, fo);
-        else
-#pragma unroll
-          for (int k = 0; k < 4; ++k) fo[k] = ys_r[ys_at(k + 1, y + 1, x)];
-        add_flux(val, half_inv,
-                 [&](int u) { return u == 0 ? qs<L>(stc, y, x + 1, 2) : ys_r[ys_at(u, y, x)]; },
-                 [&](int u) { return u == 0 ? qc[2] : fo[u - 1]; },
-                 [&](int u) { return u == 0 ? qs<L>(stc, y + 2, x + 1, 2) : ys_r[ys_at(u, y + 2, x)]; });
-      }
-      const double jz_up = qs<L>(st, y + 1, x + 1, 3);
-#pragma unroll
-      for (int u = 0; u < S; ++u) {
-        const double c = u == 0 ? qc[3] : zprev.f[u - 1];
-        const double sum_p = dadd(c, u == 0 ? jz_up : zcur.f[u - 1]);
-        val[u] = dadd(val[u], dmul(half_inv, dsub(favg_zm[u], sum_p)));
-        favg_zm[u] = sum_p;
-      }
-      // fix_negzero: the re-used z- term can only differ from the reference's
-      // in the sign of an exact zero, visible solely as a -0.0 result whose
-      // lower neighbour holds -0.0 in the same unknown (then the reference
-      // adds +0.0 and ends at +0.0).  Rare: check the input in HBM.
-      bool nz = false;
-#pragma unroll
-      for (int u = 0; u < S; ++u) nz = nz | is_negzero(val[u]);
-      if (__builtin_expect(nz, 0)) {
-        const int64_t vlow = ((int64_t)(zh - 2) * E + (y + 1)) * E + (x + 1);
-#pragma unroll
-        for (int u = 0; u < S; ++u) {
-          const double qlow = L == kAoS ? qin[(pidx * VOL + vlow) * S + u] : qin[((int64_t)u * n + pidx) * VOL + vlow];
-          if (is_negzero(val[u]) && is_negzero(qlow)) val[u] = 0.0;
-        }
-      }
-      if (DIRECT) {
-        const int64_t cell = (int64_t)(zh - 2) * P * P + y * P + x;
-#pragma unroll
-        for (int u = 0; u < S; ++u) {
-          if (L == kAoS) __stcs(qout + (pidx * IVOL + cell) * S + u, val[u]);
-          else __stcs(qout + ((int64_t)u * n + pidx) * IVOL + cell, val[u]);
-        }
-      } else {
-        double* ob = outb + (g & 1) * OUTN;
-#pragma unroll
-        for (int u = 0; u < S; ++u) {
-          if (L == kAoS) ob[(y * P + x) * S + u] = val[u];
-          else ob[u * P * P + y * P + x] = val[u];
-        }
-        fence_proxy_async();
-      }
-    };
+  for (int jp = 0; jp < my_patches; ++jp) {
+    const int64_t pidx = patch_index(jp);
+    const double dx = __ddiv_rn(cell_size[pidx * 3], (double)P);   // vectorized.py:169
+    const double inv = __ddiv_rn(dtv[pidx], dx);                    // vectorized.py:170
+    const double half_inv = dmul(0.5, inv);                         // `0.5 * inv * a`
+    if (tid == 0 && !inv_ok(inv)) slow = true;
 
-    if (interior && zh >= 2 && zh <= P) {
-      // steady state: closures of plane zh and the update of plane zh-1, one block
-      closure_full();
-      update_full();
-    } else if (interior) {
-      if (full_plane) {
-        closure_full();
-      } else {   // z-halo planes: only their z-side data
+    // One plane of the march.  18 planes per patch and NST = 3 keep the ring
+    // stage / parity and the side-buffer parity (zh & 1) patch-periodic.
+    auto plane = [&](int zh, auto kind) {
+      constexpr int K = decltype(kind)::value;
+      const double* st = ring + stg * STAGE;                                // plane zh
+      const double* stc = ring + (stg == 0 ? NST - 1 : stg - 1) * STAGE;   // plane zh-1
+      double* ys_w = ysb + (zh & 1) * SIDE;
+      double* xs_w = xsb + (zh & 1) * SIDE;
+      const double* ys_r = ysb + ((zh - 1) & 1) * SIDE;
+      const double* xs_r = xsb + ((zh - 1) & 1) * SIDE;
+      mbar_wait(&bars[stg], par);
+
+      if (interior) {
+        Side<3> zcur;
         double q[S];
         load_q<L>(st, y + 1, x + 1, q);
-        bool ok;
-        const Thermo<3> T = closure_one_ranged<3>(q, cl, 2, zcur, ok);
-        bad = bad | (ok & T.bad);
-        slow = slow | !ok;
-      }
-      if (zh == 1) {
-        // only the face (0 | 1) -- the minus face of the first interior plane
-        double qc[S];
-        load_q<L>(stc, y + 1, x + 1, qc);
-        const double cz = dmul(half_inv, speed_max(zcur.lam, zprev.lam));
-#pragma unroll
-        for (int u = 0; u < S; ++u) {
-          const double qu = qs<L>(st, y + 1, x + 1, u);
-          tp[u] = dmul(cz, dsub(qu, qc[u]));
-          const double c = u == 0 ? qc[3] : zprev.f[u - 1];
-          favg_zm[u] = dadd(c, u == 0 ? qs<L>(st, y + 1, x + 1, 3) : zcur.f[u - 1]);   // j_z of plane 1
-        }
-      } else if (zh == NPL - 1) {
-        update_full();
-      }
-    } else if (full_plane) {
-      {   // halo warp: y-face halo rows (haloed y = 0, 17), interior columns
-        const int hy = lane < 16 ? 0 : E - 1;
-        double q[S];
-        load_q<L>(st, hy, x + 1, q);
-        Side<3> sh;
-        bool ok;
-        const Thermo<3> T = closure_one_ranged<3>(q, cl, 1, sh, ok);
-        bad = bad | (ok & T.bad);
-        slow = slow | !ok;
-        put_ys(ys_w, hy, x, sh);
-      }
-      {   // x-face halo columns (haloed x = 0, 17), interior rows
-        const int hx = lane < 16 ? 0 : E - 1;
-        double q[S];
-        load_q<L>(st, x + 1, hx, q);
-        Side<3> sh;
-        bool ok;
-        const Thermo<3> T = closure_one_ranged<3>(q, cl, 0, sh, ok);
-        bad = bad | (ok & T.bad);
-        slow = slow | !ok;
-        put_xs(xs_w, x, hx, sh);
-      }
-    }
-    if (zh == NPL - 1) {   // patch complete: queue it for the exact path if any lane left the range gate
-      if (__any_sync(0xffffffffu, slow) && lane == 0) atomicOr(&slowflag[jp & 1], 1u);
-      slow = false;
-    }
-    if (interior) {
-      zprev = zcur;
-      if (zh == NPL - 1) {   // patch complete: per-warp max of the wave speeds
-        unsigned long long m = cm;
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-          const unsigned long long v = __shfl_xor_sync(0xffffffffu, m, o);
+        // ---- A: closure of this column's volume of plane zh ----
+        if (K == kFirst || K == kSteady) {
+          Side<3> sd[3];
+          bool ok;
+          const Thermo<3> T = closure_all_ranged<3>(q, cl, sd, ok);
+          bad = bad | (ok & T.bad);
+          slow = slow | !ok;
+          unsigned long long m = (unsigned long long)__double_as_longlong(sd[0].lam);
+          unsigned long long v = (unsigned long long)__double_as_longlong(sd[1].lam);
           m = v > m ? v : m;
+          v = (unsigned long long)__double_as_longlong(sd[2].lam);
+          m = v > m ? v : m;
+          cm = m > cm ? m : cm;
+          put_xs(xs_w, y, x + 1, sd[0]);
+          put_ys(ys_w, y + 1, x, sd[1]);
+          zcur = sd[2];
+        } else {   // z-halo planes: only their z-side data
+          bool ok;
+          const Thermo<3> T = closure_one_ranged<3>(q, cl, 2, zcur, ok);
+          bad = bad | (ok & T.bad);
+          slow = slow | !ok;
         }
-        if (lane == 0) wmax[(jp & 1) * 8 + warp] = m;
-        cm = 0;
+        if (K == kFirst) {
+          // only the face (0 | 1) -- the minus face of the first interior plane
+          double qc[S];
+          load_q<L>(stc, y + 1, x + 1, qc);
+          const double cz = dmul(half_inv, speed_max(zcur.lam, zprev.lam));
+#pragma unroll
+          for (int u = 0; u < S; ++u) {
+            tp[u] = dmul(cz, dsub(q[u], qc[u]));
+            const double c = u == 0 ? qc[3] : zprev.f[u - 1];
+            favg_zm[u] = dadd(c, u == 0 ? q[3] : zcur.f[u - 1]);
+          }
+        }
+        // ---- B: update of this column's cell of plane zh-1 ----
+        // Plane zh-1's side data were published in the previous iteration
+        // (behind the barrier that ended it); this column's plane-zh z data are
+        // zcur.  No barrier between A and B: the steady state is one basic
+        // block the scheduler interleaves.
+        if (K == kSteady || K == kZHi) {
+          double qc[S], val[S], qn[S];
+          load_q<L>(stc, y + 1, x + 1, qc);
+          const double lx = xs_r[xs_at(0, y, x + 1)];
+          const double ly = ys_r[ys_at(0, y + 1, x)];
+          // z face (zh-1 | zh) seen from the lower cell: coeff*(Q_zh - Q_zh-1)
+          const double cz = dmul(half_inv, speed_max(zcur.lam, zprev.lam));
+#pragma unroll
+          for (int u = 0; u < S; ++u) val[u] = qc[u];                       // _pass_copy
+          // dissipation x-, x+, y-, y+ (vectorized.py:173-180)
+          load_q<L>(stc, y + 1, x, qn);
+          dissipate<3>(val, half_inv, lx, qc, xs_r[xs_at(0, y, x)], qn);
+          load_q<L>(stc, y + 1, x + 2, qn);
+          dissipate<3>(val, half_inv, lx, qc, xs_r[xs_at(0, y, x + 2)], qn);
+          load_q<L>(stc, y, x + 1, qn);
+          dissipate<3>(val, half_inv, ly, qc, ys_r[ys_at(0, y, x)], qn);
+          load_q<L>(stc, y + 2, x + 1, qn);
+          dissipate<3>(val, half_inv, ly, qc, ys_r[ys_at(0, y + 2, x)], qn);
+          // z-: the previous face's term, negated; z+: this face's term
+#pragma unroll
+          for (int u = 0; u < S; ++u) val[u] = dsub(val[u], tp[u]);
+#pragma unroll
+          for (int u = 0; u < S; ++u) {
+            tp[u] = dmul(cz, dsub(q[u], qc[u]));
+            val[u] = dadd(val[u], tp[u]);
+          }
+          // flux differences x, y, z (vectorized.py:193-200)
+          {
+            double fo[4];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) fo[k] = xs_r[xs_at(k + 1, y, x + 1)];
+            add_flux(val, half_inv,
+                     [&](int u) { return u == 0 ? qs<L>(stc, y + 1, x, 1) : xs_r[xs_at(u, y, x)]; },
+                     [&](int u) { return u == 0 ? qc[1] : fo[u - 1]; },
+                     [&](int u) { return u == 0 ? qs<L>(stc, y + 1, x + 2, 1) : xs_r[xs_at(u, y, x + 2)]; });
+          }
+          {
+            double fo[4];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) fo[k] = ys_r[ys_at(k + 1, y + 1, x)];
+            add_flux(val, half_inv,
+                     [&](int u) { return u == 0 ? qs<L>(stc, y, x + 1, 2) : ys_r[ys_at(u, y, x)]; },
+                     [&](int u) { return u == 0 ? qc[2] : fo[u - 1]; },
+                     [&](int u) { return u == 0 ? qs<L>(stc, y + 2, x + 1, 2) : ys_r[ys_at(u, y + 2, x)]; });
+          }
+#pragma unroll
+          for (int u = 0; u < S; ++u) {
+            const double c = u == 0 ? qc[3] : zprev.f[u - 1];
+            const double sum_p = dadd(c, u == 0 ? q[3] : zcur.f[u - 1]);
+            val[u] = dadd(val[u], dmul(half_inv, dsub(favg_zm[u], sum_p)));
+            favg_zm[u] = sum_p;
+          }
+          // fix_negzero: the re-used z- term can only differ from the reference's
+          // in the sign of an exact zero, visible solely as a -0.0 result whose
+          // lower neighbour holds -0.0 in the same unknown (then the reference
+          // adds +0.0 and ends at +0.0).  Rare: check the input in HBM.
+          bool nz = false;
+#pragma unroll
+          for (int u = 0; u < S; ++u) nz = nz | is_negzero(val[u]);
+          if (__builtin_expect(nz, 0)) {
+            const int64_t vlow = ((int64_t)(zh - 2) * E + (y + 1)) * E + (x + 1);
+#pragma unroll
+            for (int u = 0; u < S; ++u) {
+              const double qlow =
+                  L == kAoS ? qin[(pidx * VOL + vlow) * S + u] : qin[((int64_t)u * n + pidx) * VOL + vlow];
+              if (is_negzero(val[u]) && is_negzero(qlow)) val[u] = 0.0;
+            }
+          }
+          double* ob = outb + (zh & 1) * OUTN;   // output buffer of interior plane zh-2 (parity (zh-2)&1)
+#pragma unroll
+          for (int u = 0; u < S; ++u) {
+            if (L == kAoS) ob[(y * P + x) * S + u] = val[u];
+            else ob[u * P * P + y * P + x] = val[u];
+          }
+          fence_proxy_async();
+        }
+        zprev = zcur;
+      } else if (K == kFirst || K == kSteady) {
+        // the halo warp: face-halo volumes of plane zh, only their face-normal side data
+        {   // y-face halo rows (haloed y = 0, 17), interior columns
+          const int hy = lane < 16 ? 0 : E - 1;
+          double qh[S];
+          load_q<L>(st, hy, x + 1, qh);
+          Side<3> sh;
+          bool ok;
+          const Thermo<3> T = closure_one_ranged<3>(qh, cl, 1, sh, ok);
+          bad = bad | (ok & T.bad);
+          slow = slow | !ok;
+          put_ys(ys_w, hy, x, sh);
+        }
+        {   // x-face halo columns (haloed x = 0, 17), interior rows
+          const int hx = lane < 16 ? 0 : E - 1;
+          double qh[S];
+          load_q<L>(st, x + 1, hx, qh);
+          Side<3> sh;
+          bool ok;
+          const Thermo<3> T = closure_one_ranged<3>(qh, cl, 0, sh, ok);
+          bad = bad | (ok & T.bad);
+          slow = slow | !ok;
+          put_xs(xs_w, x, hx, sh);
+        }
       }
-    }
-    // One barrier per plane: publishes this plane's side data and output, and
-    // retires plane zh-1's stage and side buffers for reuse.
-    if (!DIRECT && producer) bulk_wait_read0();   // output buffer (g+1)&1, written next iteration, is free
-    __syncthreads();
-    if (producer) {
-      if (g + NST - 1 < G) issue(g + NST - 1);   // into the stage of plane g-1, retired just now
-      if (!DIRECT && zh >= 2) store_out(g);
-      if (zh == NPL - 1) finish_patch_max(jp);
-    }
-    stg = stg == NST - 1 ? 0 : stg + 1;
-    par ^= (stg == 0);
-    if (++zh == NPL) {
-      zh = 0;
-      ++jp;
-      pidx += gridDim.x;
-    }
+      if (K == kZHi) {   // patch complete
+        if (__any_sync(0xffffffffu, slow) && lane == 0) atomicOr(&slowflag[jp & 1], 1u);
+        slow = false;
+        if (interior) {   // per-warp max of the wave speeds
+          unsigned long long m = cm;
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) {
+            const unsigned long long v = __shfl_xor_sync(0xffffffffu, m, o);
+            m = v > m ? v : m;
+          }
+          if (lane == 0) wmax[(jp & 1) * 8 + warp] = m;
+          cm = 0;
+        }
+      }
+      // One barrier per plane: publishes this plane's side data and output, and
+      // retires plane zh-1's ring stage and side buffers for reuse.
+      if (producer) bulk_wait_read0();   // output buffer (zh+1)&1, written next iteration, is free
+      __syncthreads();
+      if (producer) {
+        // plane zh+2 (of this or the next patch) into the stage of plane zh-1, retired just now
+        const int zn = zh + 2 < NPL ? zh + 2 : zh + 2 - NPL;
+        const int jn = zh + 2 < NPL ? jp : jp + 1;
+        if (jn < my_patches) issue(jn, zn, stg == 0 ? NST - 1 : stg - 1);
+        if (K == kSteady || K == kZHi) store_out(pidx, zh - 2);
+        if (K == kZHi) finish_patch_max(jp, pidx);
+      }
+      stg = stg == NST - 1 ? 0 : stg + 1;
+      par ^= (stg == 0);
+    };
+
+    plane(0, Kind<kZLo>{});
+    plane(1, Kind<kFirst>{});
+#pragma unroll 1
+    for (int zh = 2; zh <= P; ++zh) plane(zh, Kind<kSteady>{});
+    plane(NPL - 1, Kind<kZHi>{});
   }
 
-  if (USE_TMEM) tmem_fence_before();
   const int any_bad = __syncthreads_or(bad ? 1 : 0);
-  if (USE_TMEM) {
-    tmem_fence_after();
-    if (warp == 0) tmem_dealloc(*tmem_slot, TMEM_COLS);
-  }
   if (producer) bulk_wait_all0();
   if (tid == 0 && any_bad) atomicOr(status, 1u);
 }
@@ -500,12 +438,12 @@ cudaError_t launch_impl(const FvbArgs& a, cudaStream_t st) {
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   int per_sm = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kfn, 288, BYTES);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kfn, NTHREADS, BYTES);
   if (per_sm < 1) per_sm = 1;
   int64_t grid = (int64_t)sms * per_sm;
   if (grid > a.n) grid = a.n;
   const Closure cl{a.gamma, a.gamma - 1.0};
-  kfn<<<(unsigned)grid, 288, BYTES, st>>>(a.qin, a.qout, a.cell_size, a.dt, a.max_eig, a.status, a.n, cl);
+  kfn<<<(unsigned)grid, NTHREADS, BYTES, st>>>(a.qin, a.qout, a.cell_size, a.dt, a.max_eig, a.status, a.n, cl);
   return cudaGetLastError();
 }
 

@@ -23,6 +23,8 @@ struct FvbArgs {
 cudaError_t fvb_launch_generic(const FvbArgs& a, cudaStream_t st);
 cudaError_t fvb_launch_fused16(const FvbArgs& a, cudaStream_t st);
 cudaError_t fvb_launch_fused3d16(const FvbArgs& a, cudaStream_t st);
+cudaError_t fvb_launch_fused3d16_half(const FvbArgs& a, cudaStream_t st);
+bool fvb_fused3d_use_half();
 cudaError_t fvb_launch_redo(const FvbArgs& a, cudaStream_t st);
 bool fvb_fused16_supported(int dim, int p, int layout);
 bool fvb_small3d_supported(int dim, int p, int layout);

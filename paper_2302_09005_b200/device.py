@@ -86,7 +86,8 @@ class DeviceBatch:
         self.dt = torch.zeros(self.n_patches, **f64)
         self.max_eigenvalue = torch.zeros(self.n_patches, **f64)
         # status[0]: non-physical flag; status[1], status[2..]: redo list (include/fvb200.h)
-        self.status = torch.zeros(self.n_patches + 2, dtype=torch.int32, device=self.device)
+        self.status = torch.zeros(int(_lib.load().fvb_status_words(self.n_patches)), dtype=torch.int32,
+                                  device=self.device)
 
     # -- construction / transfer ---------------------------------------------------------------
     @classmethod
