@@ -342,12 +342,24 @@ bool fvb_fused3d_use_half() {
   return v == 1;
 }
 
+// 2D p=16 AoS kernel choice: warp-autonomous y march (default) or the block
+// kernel above (FVB_2D_KERNEL=block, kept for A/B measurements; always used for SoA).
+bool fvb_fused2d_use_warp() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("FVB_2D_KERNEL");
+    v = (e && e[0] == 'b') ? 0 : 1;
+  }
+  return v == 1;
+}
+
 cudaError_t fvb_launch_fused16(const FvbArgs& a, cudaStream_t st) {
   using namespace fvb;
   if (a.n <= 0) return cudaSuccess;
   if (a.p != 16) return fvb_launch_small3d(a, st);   // includes its redo pass
   cudaError_t e;
   if (a.dim == 3) e = fvb_fused3d_use_half() ? fvb_launch_fused3d16_half(a, st) : fvb_launch_fused3d16(a, st);
+  else if (a.layout == kAoS && fvb_fused2d_use_warp()) e = fvb_launch_fused2d16_warp(a, st);
   else e = a.layout == kAoS ? f2::launch<kAoS>(a, st) : f2::launch<kSoA>(a, st);
   if (e != cudaSuccess) return e;
   return fvb_launch_redo(a, st);   // exact re-evaluation of queued patches (usually none)

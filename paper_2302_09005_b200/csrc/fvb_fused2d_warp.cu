@@ -1,0 +1,341 @@
+// fvb_fused2d_warp.cu -- fused 2D Rusanov patch update for p = 16, warp-autonomous y march.
+//
+// Each warp owns TWO patches at a time (lane l -> patch slot l & 1, column
+// x = l >> 1) and marches them row by row in y, exactly like the 3D kernels
+// march planes in z:
+//
+//   * the y faces are evaluated once and re-used (negated) by the upper cell,
+//     the y-side data and the face carries live in registers;
+//   * x neighbours are exchanged through a per-warp shared-memory row buffer,
+//     so the only synchronisation is __syncwarp -- no CTA barrier at all;
+//   * haloed rows stream through a per-warp ring of TMA bulk-copy stages
+//     (one 576 B row of each patch per stage, mbarrier complete_tx), issued
+//     by lane 0 as soon as a row retires;
+//   * the x-face halo columns (hx = 0, 17) are evaluated two rows at a time by
+//     eight lanes;
+//   * output rows are staged in shared memory and written back with TMA bulk
+//     stores (one 512 B row per patch).
+//
+// Shared-memory layout per warp is bank-conflict free for the 32-byte AoS
+// volumes: the two patches' rows are offset by 16 B modulo 128 B, so a
+// quarter-warp's eight 16-byte LDS.128 accesses hit eight distinct bank
+// quads.  (The block kernel in fvb_fused2d.cu reads 32-byte-strided LDS.64
+// with 4-way conflicts.)
+//
+// Arithmetic: the reference's operation order, bit for bit (fvb_exact.cuh);
+// the re-used y face differs from the reference only in the sign of an exact
+// zero, repaired exactly as in fvb_fused3d.cu (fix_negzero).  AoS only (the
+// packed SoA layout uses the block kernel).
+#include <cuda_runtime.h>
+
+#include "fvb_exact.cuh"
+#include "fvb_kernels.h"
+#include "fvb_layout.cuh"
+#include "fvb_tma.cuh"
+
+namespace fvb {
+namespace f2w {
+
+using namespace f16;
+
+constexpr int P = 16, E = 18, S = 4;
+constexpr int64_t VOL = (int64_t)E * E;
+constexpr int64_t IVOL = (int64_t)P * P;
+constexpr int ROWD = E * S;               // doubles per haloed patch row (576 B)
+constexpr int OFFB = 82;                  // patch-B row offset in a stage: 656 B = 16 mod 128
+constexpr int STGD = 160;                 // stage: two rows + padding (1,280 B)
+constexpr int NS = 6;                     // ring stages per warp
+constexpr int HB = 2;                     // halo-column rows per batch (8 lanes)
+constexpr int XSD = 4 * 32;               // x-side row: [c][lane]
+constexpr int HXS = 4 * P * 4;            // halo x-side: [c][row 1..16][side][slot]
+constexpr int OUTR = P * S;               // one output row of one patch (512 B)
+constexpr int OFFO = 66;                  // patch-B output offset: 528 B = 16 mod 128
+constexpr int OUTD = 136;                 // output staging per row parity
+constexpr int WPC = 4;                    // warps per CTA
+constexpr int W_RING = 0;
+constexpr int W_XS = W_RING + NS * STGD;
+constexpr int W_HX = W_XS + 2 * XSD;
+constexpr int W_OUT = W_HX + HXS;
+constexpr int W_BAR = W_OUT + 2 * OUTD;
+constexpr int WARPD = W_BAR + NS + 2;     // doubles per warp (16 B multiple)
+constexpr size_t BYTES = (size_t)WPC * WARPD * 8;
+
+__device__ __forceinline__ void lds_q(const double* p, double (&q)[S]) {
+  const double2 a = *reinterpret_cast<const double2*>(p);
+  const double2 b = *reinterpret_cast<const double2*>(p + 2);
+  q[0] = a.x; q[1] = a.y; q[2] = b.x; q[3] = b.y;
+}
+__device__ __forceinline__ void sts_q(double* p, const double (&q)[S]) {
+  *reinterpret_cast<double2*>(p) = make_double2(q[0], q[1]);
+  *reinterpret_cast<double2*>(p + 2) = make_double2(q[2], q[3]);
+}
+__device__ __forceinline__ bool inv_ok(double inv) {
+  const unsigned e = ((unsigned)__double2hiint(inv) >> 20) & 0x7ffu;
+  return inv == 0.0 || (e >= 2u && e < 0x7ffu);
+}
+__device__ __forceinline__ bool is_negzero(double v) {
+  return (unsigned long long)__double_as_longlong(v) == 0x8000000000000000ull;
+}
+
+__global__ void __launch_bounds__(WPC * 32)
+fused2d_warp_kernel(const double* __restrict__ qin, double* __restrict__ qout, const double* __restrict__ cell_size,
+                    const double* __restrict__ dtv, double* __restrict__ max_eig, unsigned* __restrict__ status,
+                    int64_t n, Closure cl) {
+  extern __shared__ __align__(128) double sm[];
+  const int warp = threadIdx.x >> 5, l = threadIdx.x & 31;
+  double* wb = sm + warp * WARPD;
+  double* ring = wb + W_RING;
+  double* xsb = wb + W_XS;
+  double* hxs = wb + W_HX;
+  double* outb = wb + W_OUT;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(wb + W_BAR);
+
+  const int ps = l & 1;          // patch slot
+  const int x = l >> 1;          // interior column 0..15
+  const int64_t items = (n + 1) >> 1;
+  const int64_t gw = (int64_t)blockIdx.x * WPC + warp;
+  const int64_t tw = (int64_t)gridDim.x * WPC;
+  const int my_items = items > gw ? (int)((items - 1 - gw) / tw + 1) : 0;
+  const int rows_total = my_items * E;
+
+  // haloed row hy of this warp's j-th item into stage s (lane 0)
+  auto issue = [&](int rr) {
+    const int j = rr / E, hy = rr - j * E;
+    const int64_t pa = 2 * (gw + (int64_t)j * tw);
+    const bool vb = pa + 1 < n;
+    const int s = rr % NS;
+    double* st = ring + s * STGD;
+    uint64_t* bar = bars + s;
+    fence_proxy_async();
+    mbar_expect_tx(bar, (uint32_t)((vb ? 2 : 1) * ROWD * 8));
+    tma_load_1d(st, qin + (pa * VOL + hy * E) * S, (uint32_t)(ROWD * 8), bar);
+    if (vb) tma_load_1d(st + OFFB, qin + ((pa + 1) * VOL + hy * E) * S, (uint32_t)(ROWD * 8), bar);
+  };
+
+  if (l == 0) {
+#pragma unroll
+    for (int s = 0; s < NS; ++s) mbar_init(&bars[s], 1);
+    fence_mbar_init();
+  }
+  __syncwarp();
+  if (l == 0)
+    for (int rr = 0; rr < NS && rr < rows_total; ++rr) issue(rr);   // the whole ring; row r+NS refills r
+
+  bool bad = false;
+  int rr = 0;   // warp-global row counter (ring stage rr % NS, phase parity (rr / NS) & 1)
+  for (int j = 0; j < my_items; ++j) {
+    const int64_t pa = 2 * (gw + (int64_t)j * tw);
+    const int64_t pidx = pa + ps;
+    const bool valid = pidx < n;
+    const int64_t pl = valid ? pidx : pa;   // invalid slot mirrors patch A's scalars (results discarded)
+    const double dx = __ddiv_rn(cell_size[pl * 2], (double)P);   // vectorized.py:169
+    const double inv = __ddiv_rn(dtv[pl], dx);                    // vectorized.py:170
+    const double half_inv = dmul(0.5, inv);
+    bool slow = !inv_ok(inv);
+    unsigned long long cm = 0;
+
+    // y-march carries (row hy-1): own state and x-side data, y-side data,
+    // the previous y face's dissipation term tp and unscaled flux sum favg
+    double oq[S], olx = 0.0, ofx[3] = {0.0, 0.0, 0.0};
+    Side<2> yprev;
+    double tp[S], favg[S];
+#pragma unroll
+    for (int u = 0; u < S; ++u) { oq[u] = 0.0; tp[u] = 0.0; favg[u] = 0.0; }
+    yprev.lam = 0.0;
+#pragma unroll
+    for (int k = 0; k < 3; ++k) yprev.f[k] = 0.0;
+
+    for (int hy = 0; hy < E; ++hy, ++rr) {
+      const int s = rr % NS;
+      const double* st = ring + s * STGD + ps * OFFB;                   // row hy of this lane's patch
+      const double* stp = ring + ((rr + NS - 1) % NS) * STGD + ps * OFFB;   // row hy-1
+      mbar_wait(&bars[s], (unsigned)(rr / NS) & 1u);
+
+      // ---- halo columns hx = 0, 17 of rows hy, hy+1 (x-side data only) ----
+      if ((hy & 1) && hy < E - 1) {
+        const int r2 = rr + 1;
+        mbar_wait(&bars[r2 % NS], (unsigned)(r2 / NS) & 1u);
+        if (l < 8) {
+          const int hps = l & 1, side = (l >> 1) & 1, dr = l >> 2;
+          const double* hst = ring + ((rr + dr) % NS) * STGD + hps * OFFB;
+          double qh[S];
+          lds_q(hst + (side ? E - 1 : 0) * S, qh);
+          Side<2> sh;
+          bool ok;
+          const Thermo<2> T = closure_one_ranged<2>(qh, cl, 0, sh, ok);
+          const bool hv = pa + hps < n;
+          bad = bad | (hv & ok & T.bad);
+          const int idx = ((hy + dr - 1) * 2 + side) * 2 + hps;
+          hxs[0 * 64 + idx] = sh.lam;
+#pragma unroll
+          for (int k = 0; k < 3; ++k) hxs[(k + 1) * 64 + idx] = sh.f[k];
+          // a halo volume outside the range gate invalidates its patch: the
+          // lane (< 8) with the same slot carries it into the per-patch vote
+          const unsigned m = __ballot_sync(0xffu, !ok);
+          slow = slow | ((m & (ps ? 0xaau : 0x55u)) != 0u);
+        }
+      }
+
+      // ---- closure of this lane's volume of row hy ----
+      Side<2> ycur;
+      double q[S];
+      lds_q(st + (x + 1) * S, q);
+      double nlx = 0.0, nfx[3] = {0.0, 0.0, 0.0};
+      if (hy >= 1 && hy <= P) {
+        Side<2> sd[2];
+        bool ok;
+        const Thermo<2> T = closure_all_ranged<2>(q, cl, sd, ok);
+        bad = bad | (valid & ok & T.bad);
+        slow = slow | !ok;
+        const unsigned long long a = (unsigned long long)__double_as_longlong(sd[0].lam);
+        const unsigned long long b = (unsigned long long)__double_as_longlong(sd[1].lam);
+        const unsigned long long m = a > b ? a : b;
+        cm = m > cm ? m : cm;
+        double* xw = xsb + (hy & 1) * XSD;
+        xw[0 * 32 + l] = sd[0].lam;
+#pragma unroll
+        for (int k = 0; k < 3; ++k) xw[(k + 1) * 32 + l] = sd[0].f[k];
+        nlx = sd[0].lam;
+#pragma unroll
+        for (int k = 0; k < 3; ++k) nfx[k] = sd[0].f[k];
+        ycur = sd[1];
+      } else {   // y-face halo rows: only their y-side data
+        bool ok;
+        const Thermo<2> T = closure_one_ranged<2>(q, cl, 1, ycur, ok);
+        bad = bad | (valid & ok & T.bad);
+        slow = slow | !ok;
+      }
+      __syncwarp();   // x-side row hy and the halo batch are visible to the warp
+
+      if (hy == 1) {
+        // the face (0 | 1): minus face of the first interior row
+        const double cy = dmul(half_inv, speed_max(ycur.lam, yprev.lam));
+#pragma unroll
+        for (int u = 0; u < S; ++u) {
+          tp[u] = dmul(cy, dsub(q[u], oq[u]));
+          const double c = u == 0 ? oq[2] : yprev.f[u - 1];
+          favg[u] = dadd(c, u == 0 ? q[2] : ycur.f[u - 1]);
+        }
+      } else if (hy >= 2) {
+        // ---- update of this lane's cell of row hy-1 (interior row hy-2) ----
+        const double* xr = xsb + ((hy - 1) & 1) * XSD;
+        const int hrow = ((hy - 2) * 2) * 2 + ps;   // halo index of row hy-1, side 0
+        double val[S], qn[S];
+#pragma unroll
+        for (int u = 0; u < S; ++u) val[u] = oq[u];                        // _pass_copy
+        // x- face
+        lds_q(stp + x * S, qn);
+        const double* ml = x == 0 ? hxs + hrow : xr + (l - 2);
+        const int mstride = x == 0 ? 64 : 32;
+        const double jl = qn[1];
+        dissipate<2>(val, half_inv, olx, oq, ml[0], qn);
+        // x+ face
+        lds_q(stp + (x + 2) * S, qn);
+        const double* mr = x == P - 1 ? hxs + hrow + 2 : xr + (l + 2);
+        const int rstride = x == P - 1 ? 64 : 32;
+        const double jr = qn[1];
+        dissipate<2>(val, half_inv, olx, oq, mr[0], qn);
+        // y-: the previous face's term, negated; y+: this face's term
+        const double cy = dmul(half_inv, speed_max(ycur.lam, yprev.lam));
+#pragma unroll
+        for (int u = 0; u < S; ++u) val[u] = dsub(val[u], tp[u]);
+#pragma unroll
+        for (int u = 0; u < S; ++u) {
+          tp[u] = dmul(cy, dsub(q[u], oq[u]));
+          val[u] = dadd(val[u], tp[u]);
+        }
+        // flux differences x, y (vectorized.py:193-200), see fvb_fused3d.cu add_flux
+#pragma unroll
+        for (int u = 0; u < S; ++u) {
+          const double fm = u == 0 ? jl : ml[u * mstride];
+          const double fc = u == 0 ? oq[1] : ofx[u - 1];
+          const double fp = u == 0 ? jr : mr[u * rstride];
+          val[u] = dadd(val[u], dmul(half_inv, dsub(dadd(fm, fc), dadd(fc, fp))));
+        }
+#pragma unroll
+        for (int u = 0; u < S; ++u) {
+          const double c = u == 0 ? oq[2] : yprev.f[u - 1];
+          const double sum_p = dadd(c, u == 0 ? q[2] : ycur.f[u - 1]);
+          val[u] = dadd(val[u], dmul(half_inv, dsub(favg[u], sum_p)));
+          favg[u] = sum_p;
+        }
+        // fix_negzero (fvb_fused3d.cu): a -0.0 result whose lower neighbour
+        // holds -0.0 in that unknown is +0.0 in the reference
+        bool nz = false;
+#pragma unroll
+        for (int u = 0; u < S; ++u) nz = nz | is_negzero(val[u]);
+        if (__builtin_expect(nz, 0)) {
+#pragma unroll
+          for (int u = 0; u < S; ++u) {
+            const double qlow = qin[(pl * VOL + (int64_t)(hy - 2) * E + (x + 1)) * S + u];
+            if (is_negzero(val[u]) && is_negzero(qlow)) val[u] = 0.0;
+          }
+        }
+        // stage the output row; the buffer of this parity was last stored two rows ago
+        if (l == 0) bulk_wait_read<1>();
+        __syncwarp();
+        double* ob = outb + (hy & 1) * OUTD;
+        sts_q(ob + ps * OFFO + x * S, val);
+        fence_proxy_async();
+        __syncwarp();
+        if (l == 0) {
+          const int z = hy - 2;
+          tma_store_1d(qout + (pa * IVOL + z * P) * S, ob, (uint32_t)(OUTR * 8));
+          if (pa + 1 < n) tma_store_1d(qout + ((pa + 1) * IVOL + z * P) * S, ob + OFFO, (uint32_t)(OUTR * 8));
+          bulk_commit();
+        }
+      }
+      if (rr >= 1) {
+        __syncwarp();   // row rr-1 (this item's row hy-1, or the last item's row 17) consumed: refill its stage
+        if (l == 0 && rr - 1 + NS < rows_total) issue(rr - 1 + NS);
+      }
+#pragma unroll
+      for (int u = 0; u < S; ++u) oq[u] = q[u];
+      olx = nlx;
+#pragma unroll
+      for (int k = 0; k < 3; ++k) ofx[k] = nfx[k];
+      yprev = ycur;
+    }
+
+    // ---- per-patch results: max wave speed (vectorized.py:226-231), redo queue ----
+#pragma unroll
+    for (int o = 2; o < 32; o <<= 1) {
+      const unsigned long long v = __shfl_xor_sync(0xffffffffu, cm, o);
+      cm = v > cm ? v : cm;
+    }
+    const unsigned sm_ = __ballot_sync(0xffffffffu, slow);
+    if (l < 2 && valid) {
+      max_eig[pidx] = __longlong_as_double((long long)cm);
+      if (sm_ & (ps ? 0xaaaaaaaau : 0x55555555u)) {
+        const unsigned k = atomicAdd(&status[1], 1u);
+        status[2 + k] = (unsigned)pidx;
+      }
+    }
+  }
+  if (l == 0) bulk_wait_all0();
+  if (__any_sync(0xffffffffu, bad) && l == 0) atomicOr(status, 1u);
+}
+
+}  // namespace f2w
+}  // namespace fvb
+
+cudaError_t fvb_launch_fused2d16_warp(const FvbArgs& a, cudaStream_t st) {
+  using namespace fvb::f2w;
+  if (a.n <= 0) return cudaSuccess;
+  auto kfn = fused2d_warp_kernel;
+  cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)BYTES);
+  if (e != cudaSuccess) return e;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  int per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kfn, WPC * 32, BYTES);
+  if (per_sm < 1) per_sm = 1;
+  const int64_t items = (a.n + 1) / 2;
+  int64_t grid = (int64_t)sms * per_sm;
+  const int64_t need = (items + WPC - 1) / WPC;
+  if (grid > need) grid = need;
+  const fvb::Closure cl{a.gamma, a.gamma - 1.0};
+  kfn<<<(unsigned)grid, WPC * 32, BYTES, st>>>(a.qin, a.qout, a.cell_size, a.dt, a.max_eig, a.status, a.n, cl);
+  return cudaGetLastError();
+}

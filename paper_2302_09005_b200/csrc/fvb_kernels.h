@@ -25,6 +25,8 @@ cudaError_t fvb_launch_fused16(const FvbArgs& a, cudaStream_t st);
 cudaError_t fvb_launch_fused3d16(const FvbArgs& a, cudaStream_t st);
 cudaError_t fvb_launch_fused3d16_half(const FvbArgs& a, cudaStream_t st);
 bool fvb_fused3d_use_half();
+cudaError_t fvb_launch_fused2d16_warp(const FvbArgs& a, cudaStream_t st);
+bool fvb_fused2d_use_warp();
 cudaError_t fvb_launch_redo(const FvbArgs& a, cudaStream_t st);
 bool fvb_fused16_supported(int dim, int p, int layout);
 bool fvb_small3d_supported(int dim, int p, int layout);
