@@ -43,21 +43,27 @@ constexpr int64_t VOL = (int64_t)E * E;
 constexpr int64_t IVOL = (int64_t)P * P;
 constexpr int ROWD = E * S;               // doubles per haloed patch row (576 B)
 constexpr int OFFB = 82;                  // patch-B row offset in a stage: 656 B = 16 mod 128
-constexpr int STGD = 160;                 // stage: two rows + padding (1,280 B)
-constexpr int NS = 6;                     // ring stages per warp
-constexpr int HB = 2;                     // halo-column rows per batch (8 lanes)
+constexpr int STGD = 154;                 // stage: two rows + padding (1,232 B)
+constexpr int NS = 7;                     // ring stages per warp
+constexpr int HB = 4;                     // halo-column rows per batch (16 lanes)
 constexpr int XSD = 4 * 32;               // x-side row: [c][lane]
-constexpr int HXS = 4 * P * 4;            // halo x-side: [c][row 1..16][side][slot]
+constexpr int HXR = 8;                    // halo x-side ring rows
+constexpr int HXC = HXR * 4;              // halo x-side doubles per component: [row slot][side][patch slot]
+constexpr int HXS = 4 * HXC;              // [c][row slot][side][patch slot]
 constexpr int OUTR = P * S;               // one output row of one patch (512 B)
 constexpr int OFFO = 66;                  // patch-B output offset: 528 B = 16 mod 128
 constexpr int OUTD = 136;                 // output staging per row parity
 constexpr int WPC = 4;                    // warps per CTA
+#ifndef FVB2D_HY_UNROLL
+#define FVB2D_HY_UNROLL 2
+#endif
+constexpr int HY_UNROLL = FVB2D_HY_UNROLL;
 constexpr int W_RING = 0;
 constexpr int W_XS = W_RING + NS * STGD;
 constexpr int W_HX = W_XS + 2 * XSD;
 constexpr int W_OUT = W_HX + HXS;
 constexpr int W_BAR = W_OUT + 2 * OUTD;
-constexpr int WARPD = W_BAR + NS + 2;     // doubles per warp (16 B multiple)
+constexpr int WARPD = (W_BAR + NS + 1) & ~1;   // doubles per warp (16 B multiple)
 constexpr size_t BYTES = (size_t)WPC * WARPD * 8;
 
 __device__ __forceinline__ void lds_q(const double* p, double (&q)[S]) {
@@ -98,31 +104,47 @@ fused2d_warp_kernel(const double* __restrict__ qin, double* __restrict__ qout, c
   const int my_items = items > gw ? (int)((items - 1 - gw) / tw + 1) : 0;
   const int rows_total = my_items * E;
 
-  // haloed row hy of this warp's j-th item into stage s (lane 0)
-  auto issue = [&](int rr) {
-    const int j = rr / E, hy = rr - j * E;
-    const int64_t pa = 2 * (gw + (int64_t)j * tw);
-    const bool vb = pa + 1 < n;
-    const int s = rr % NS;
-    double* st = ring + s * STGD;
-    uint64_t* bar = bars + s;
+  // Lane 0's issue cursor: the next haloed row to load (item ij, row ihy) and
+  // its ring stage / patch pair, advanced incrementally (no divisions).
+  int ij = 0, ihy = 0, is = 0, iissued = 0;
+  int64_t ipa = 2 * gw;
+  auto issue_next = [&]() {
+    const bool vb = ipa + 1 < n;
+    double* st = ring + is * STGD;
+    uint64_t* bar = bars + is;
     fence_proxy_async();
     mbar_expect_tx(bar, (uint32_t)((vb ? 2 : 1) * ROWD * 8));
-    tma_load_1d(st, qin + (pa * VOL + hy * E) * S, (uint32_t)(ROWD * 8), bar);
-    if (vb) tma_load_1d(st + OFFB, qin + ((pa + 1) * VOL + hy * E) * S, (uint32_t)(ROWD * 8), bar);
+    tma_load_1d(st, qin + (ipa * VOL + ihy * E) * S, (uint32_t)(ROWD * 8), bar);
+    if (vb) tma_load_1d(st + OFFB, qin + ((ipa + 1) * VOL + ihy * E) * S, (uint32_t)(ROWD * 8), bar);
+    ++iissued;
+    is = is == NS - 1 ? 0 : is + 1;
+    if (++ihy == E) {
+      ihy = 0;
+      ++ij;
+      ipa += 2 * tw;
+    }
   };
 
   if (l == 0) {
 #pragma unroll
-    for (int s = 0; s < NS; ++s) mbar_init(&bars[s], 1);
+    for (int k = 0; k < NS; ++k) mbar_init(&bars[k], 1);
     fence_mbar_init();
   }
   __syncwarp();
   if (l == 0)
-    for (int rr = 0; rr < NS && rr < rows_total; ++rr) issue(rr);   // the whole ring; row r+NS refills r
+    while (iissued < NS && iissued < rows_total) issue_next();   // the whole ring; row r+NS refills r
+
+  // per-lane constant offsets
+  const int own = ps * OFFB + (x + 1) * S;          // this lane's volume in a stage
+  const int left = ps * OFFB + x * S;               // x-1 neighbour
+  const int right = ps * OFFB + (x + 2) * S;        // x+1 neighbour
+  const bool lh = x == 0, rh = x == P - 1;          // neighbour is a face-halo column
+  const int lcs = lh ? HXC : 32, rcs = rh ? HXC : 32;   // component strides of the neighbours' x-side data
 
   bool bad = false;
-  int rr = 0;   // warp-global row counter (ring stage rr % NS, phase parity (rr / NS) & 1)
+  int s = 0;          // ring stage of the current row
+  unsigned par = 0;   // its mbarrier phase parity
+  int done = 0;       // rows consumed (refill trigger)
   for (int j = 0; j < my_items; ++j) {
     const int64_t pa = 2 * (gw + (int64_t)j * tw);
     const int64_t pidx = pa + ps;
@@ -145,19 +167,23 @@ fused2d_warp_kernel(const double* __restrict__ qin, double* __restrict__ qout, c
 #pragma unroll
     for (int k = 0; k < 3; ++k) yprev.f[k] = 0.0;
 
-    for (int hy = 0; hy < E; ++hy, ++rr) {
-      const int s = rr % NS;
-      const double* st = ring + s * STGD + ps * OFFB;                   // row hy of this lane's patch
-      const double* stp = ring + ((rr + NS - 1) % NS) * STGD + ps * OFFB;   // row hy-1
-      mbar_wait(&bars[s], (unsigned)(rr / NS) & 1u);
+#pragma unroll HY_UNROLL
+    for (int hy = 0; hy < E; ++hy) {
+      const double* st = ring + s * STGD;                         // row hy
+      const double* stp = ring + (s == 0 ? NS - 1 : s - 1) * STGD;   // row hy-1
+      mbar_wait(&bars[s], par);
 
-      // ---- halo columns hx = 0, 17 of rows hy, hy+1 (x-side data only) ----
-      if ((hy & 1) && hy < E - 1) {
-        const int r2 = rr + 1;
-        mbar_wait(&bars[r2 % NS], (unsigned)(r2 / NS) & 1u);
-        if (l < 8) {
+      // ---- halo columns hx = 0, 17 of rows hy .. hy+3 (x-side data only) ----
+      if ((hy & 3) == 1 && hy < E - 1) {
+#pragma unroll
+        for (int d = 1; d < HB; ++d) {
+          const int sd = s + d;
+          mbar_wait(&bars[sd >= NS ? sd - NS : sd], par ^ (sd >= NS ? 1u : 0u));
+        }
+        if (l < 16) {
           const int hps = l & 1, side = (l >> 1) & 1, dr = l >> 2;
-          const double* hst = ring + ((rr + dr) % NS) * STGD + hps * OFFB;
+          const int sd = s + dr;
+          const double* hst = ring + (sd >= NS ? sd - NS : sd) * STGD + hps * OFFB;
           double qh[S];
           lds_q(hst + (side ? E - 1 : 0) * S, qh);
           Side<2> sh;
@@ -165,40 +191,40 @@ fused2d_warp_kernel(const double* __restrict__ qin, double* __restrict__ qout, c
           const Thermo<2> T = closure_one_ranged<2>(qh, cl, 0, sh, ok);
           const bool hv = pa + hps < n;
           bad = bad | (hv & ok & T.bad);
-          const int idx = ((hy + dr - 1) * 2 + side) * 2 + hps;
-          hxs[0 * 64 + idx] = sh.lam;
+          const int idx = (((hy + dr - 1) & (HXR - 1)) * 2 + side) * 2 + hps;
+          hxs[0 * HXC + idx] = sh.lam;
 #pragma unroll
-          for (int k = 0; k < 3; ++k) hxs[(k + 1) * 64 + idx] = sh.f[k];
-          // a halo volume outside the range gate invalidates its patch: the
-          // lane (< 8) with the same slot carries it into the per-patch vote
-          const unsigned m = __ballot_sync(0xffu, !ok);
-          slow = slow | ((m & (ps ? 0xaau : 0x55u)) != 0u);
+          for (int k = 0; k < 3; ++k) hxs[(k + 1) * HXC + idx] = sh.f[k];
+          // a halo volume outside the range gate invalidates its patch: a lane
+          // with the same slot carries it into the per-patch vote
+          const unsigned m = __ballot_sync(0xffffu, !ok);
+          slow = slow | ((m & (ps ? 0xaaaau : 0x5555u)) != 0u);
         }
       }
 
       // ---- closure of this lane's volume of row hy ----
       Side<2> ycur;
       double q[S];
-      lds_q(st + (x + 1) * S, q);
+      lds_q(st + own, q);
       double nlx = 0.0, nfx[3] = {0.0, 0.0, 0.0};
       if (hy >= 1 && hy <= P) {
-        Side<2> sd[2];
+        Side<2> sd2[2];
         bool ok;
-        const Thermo<2> T = closure_all_ranged<2>(q, cl, sd, ok);
+        const Thermo<2> T = closure_all_ranged<2>(q, cl, sd2, ok);
         bad = bad | (valid & ok & T.bad);
         slow = slow | !ok;
-        const unsigned long long a = (unsigned long long)__double_as_longlong(sd[0].lam);
-        const unsigned long long b = (unsigned long long)__double_as_longlong(sd[1].lam);
+        const unsigned long long a = (unsigned long long)__double_as_longlong(sd2[0].lam);
+        const unsigned long long b = (unsigned long long)__double_as_longlong(sd2[1].lam);
         const unsigned long long m = a > b ? a : b;
         cm = m > cm ? m : cm;
-        double* xw = xsb + (hy & 1) * XSD;
-        xw[0 * 32 + l] = sd[0].lam;
+        double* xw = xsb + (hy & 1) * XSD + l;
+        xw[0 * 32] = sd2[0].lam;
 #pragma unroll
-        for (int k = 0; k < 3; ++k) xw[(k + 1) * 32 + l] = sd[0].f[k];
-        nlx = sd[0].lam;
+        for (int k = 0; k < 3; ++k) xw[(k + 1) * 32] = sd2[0].f[k];
+        nlx = sd2[0].lam;
 #pragma unroll
-        for (int k = 0; k < 3; ++k) nfx[k] = sd[0].f[k];
-        ycur = sd[1];
+        for (int k = 0; k < 3; ++k) nfx[k] = sd2[0].f[k];
+        ycur = sd2[1];
       } else {   // y-face halo rows: only their y-side data
         bool ok;
         const Thermo<2> T = closure_one_ranged<2>(q, cl, 1, ycur, ok);
@@ -219,20 +245,17 @@ fused2d_warp_kernel(const double* __restrict__ qin, double* __restrict__ qout, c
       } else if (hy >= 2) {
         // ---- update of this lane's cell of row hy-1 (interior row hy-2) ----
         const double* xr = xsb + ((hy - 1) & 1) * XSD;
-        const int hrow = ((hy - 2) * 2) * 2 + ps;   // halo index of row hy-1, side 0
+        const double* hr = hxs + ((hy - 2) & (HXR - 1)) * 4 + ps;   // halo x-side of row hy-1, side 0
+        const double* ml = lh ? hr : xr + (l - 2);
+        const double* mr = rh ? hr + 2 : xr + (l + 2);
         double val[S], qn[S];
 #pragma unroll
         for (int u = 0; u < S; ++u) val[u] = oq[u];                        // _pass_copy
-        // x- face
-        lds_q(stp + x * S, qn);
-        const double* ml = x == 0 ? hxs + hrow : xr + (l - 2);
-        const int mstride = x == 0 ? 64 : 32;
+        // x- face, x+ face (vectorized.py:173-180)
+        lds_q(stp + left, qn);
         const double jl = qn[1];
         dissipate<2>(val, half_inv, olx, oq, ml[0], qn);
-        // x+ face
-        lds_q(stp + (x + 2) * S, qn);
-        const double* mr = x == P - 1 ? hxs + hrow + 2 : xr + (l + 2);
-        const int rstride = x == P - 1 ? 64 : 32;
+        lds_q(stp + right, qn);
         const double jr = qn[1];
         dissipate<2>(val, half_inv, olx, oq, mr[0], qn);
         // y-: the previous face's term, negated; y+: this face's term
@@ -247,9 +270,9 @@ fused2d_warp_kernel(const double* __restrict__ qin, double* __restrict__ qout, c
         // flux differences x, y (vectorized.py:193-200), see fvb_fused3d.cu add_flux
 #pragma unroll
         for (int u = 0; u < S; ++u) {
-          const double fm = u == 0 ? jl : ml[u * mstride];
+          const double fm = u == 0 ? jl : ml[u * lcs];
           const double fc = u == 0 ? oq[1] : ofx[u - 1];
-          const double fp = u == 0 ? jr : mr[u * rstride];
+          const double fp = u == 0 ? jr : mr[u * rcs];
           val[u] = dadd(val[u], dmul(half_inv, dsub(dadd(fm, fc), dadd(fc, fp))));
         }
 #pragma unroll
@@ -285,10 +308,13 @@ fused2d_warp_kernel(const double* __restrict__ qin, double* __restrict__ qout, c
           bulk_commit();
         }
       }
-      if (rr >= 1) {
-        __syncwarp();   // row rr-1 (this item's row hy-1, or the last item's row 17) consumed: refill its stage
-        if (l == 0 && rr - 1 + NS < rows_total) issue(rr - 1 + NS);
+      if (done >= 1) {
+        __syncwarp();   // the previous row (this item's row hy-1, or the last item's row 17) is consumed
+        if (l == 0 && iissued < rows_total) issue_next();   // refills its stage
       }
+      ++done;
+      s = s == NS - 1 ? 0 : s + 1;
+      par ^= (s == 0);
 #pragma unroll
       for (int u = 0; u < S; ++u) oq[u] = q[u];
       olx = nlx;
