@@ -83,7 +83,7 @@ __device__ __forceinline__ bool is_negzero(double v) {
   return (unsigned long long)__double_as_longlong(v) == 0x8000000000000000ull;
 }
 
-__global__ void __launch_bounds__(WPC * 32)
+__global__ void __launch_bounds__(WPC * 32, 4)
 fused2d_warp_kernel(const double* __restrict__ qin, double* __restrict__ qout, const double* __restrict__ cell_size,
                     const double* __restrict__ dtv, double* __restrict__ max_eig, unsigned* __restrict__ status,
                     int64_t n, Closure cl) {
@@ -145,13 +145,29 @@ fused2d_warp_kernel(const double* __restrict__ qin, double* __restrict__ qout, c
   int s = 0;          // ring stage of the current row
   unsigned par = 0;   // its mbarrier phase parity
   int done = 0;       // rows consumed (refill trigger)
+  // per-patch scalars of item j (an invalid slot mirrors patch A; its results are discarded),
+  // loaded one item ahead so their latency never stalls the march
+  auto scalars = [&](int j, double& cs, double& dtp) {
+    cs = 1.0;
+    dtp = 0.0;
+    if (j < my_items) {
+      const int64_t pa = 2 * (gw + (int64_t)j * tw);
+      const int64_t pi = pa + ps < n ? pa + ps : pa;
+      cs = __ldg(cell_size + pi * 2);
+      dtp = __ldg(dtv + pi);
+    }
+  };
+  double cs_next, dt_next;
+  scalars(0, cs_next, dt_next);
   for (int j = 0; j < my_items; ++j) {
     const int64_t pa = 2 * (gw + (int64_t)j * tw);
     const int64_t pidx = pa + ps;
     const bool valid = pidx < n;
-    const int64_t pl = valid ? pidx : pa;   // invalid slot mirrors patch A's scalars (results discarded)
-    const double dx = __ddiv_rn(cell_size[pl * 2], (double)P);   // vectorized.py:169
-    const double inv = __ddiv_rn(dtv[pl], dx);                    // vectorized.py:170
+    const int64_t pl = valid ? pidx : pa;
+    const double cs_cur = cs_next, dt_cur = dt_next;
+    scalars(j + 1, cs_next, dt_next);
+    const double dx = __ddiv_rn(cs_cur, (double)P);   // vectorized.py:169
+    const double inv = __ddiv_rn(dt_cur, dx);          // vectorized.py:170
     const double half_inv = dmul(0.5, inv);
     bool slow = !inv_ok(inv);
     unsigned long long cm = 0;

@@ -50,12 +50,23 @@ struct Cfg {
   static constexpr size_t BYTES = (size_t)TOTAL * 8;
 };
 
-// record (direction n, component c) of the volume whose haloed coordinate along n
-// is hn and whose interior coordinates across n are (a, b): [n][c][b][a][hn]
+// Record (direction n, component c) of the volume whose haloed coordinate along
+// n is hn and whose interior coordinates across n are (a, b) -- a, b the
+// lower / higher remaining axes (x: (y, z), y: (x, z), z: (x, y)).  The layouts
+// are chosen for the thread mapping below (a half-warp = the 16 cells of one y
+// row pair (x, z) at fixed y), so every LDS.64 / STS.64 of a half-warp hits 16
+// distinct bank pairs:
+//   x records [a=y][hn=hx][b=z]   lanes vary (hx, z): hn*P + b
+//   y records [hn=hy][b=z][a=x]   lanes vary (z, x) at fixed hy: b*P + a
+//   z records [b=y][hn=hz][a=x]   lanes vary (hz, x): hn*P + a
 template <int P>
 __device__ __forceinline__ int side_at(int n, int c, int hn, int a, int b) {
   using C = Cfg<P>;
-  return ((n * C::S + c) * P + b) * P * C::E + a * C::E + hn;
+  constexpr int E = C::E;
+  const int base = (n * C::S + c) * C::LINE;
+  if (n == 0) return base + (a * E + hn) * P + b;
+  if (n == 1) return base + (hn * P + b) * P + a;
+  return base + (b * E + hn) * P + a;
 }
 
 template <int P>
@@ -83,7 +94,10 @@ small3d_kernel(const double* __restrict__ qin, double* __restrict__ qout, const 
   const int tid = threadIdx.x;
   const int lp = tid / C::IVOL;              // patch slot within the iteration
   const int cell = tid % C::IVOL;
-  const int cx = cell % P, cy = (cell / P) % P, cz = cell / (P * P);
+  // cell -> (x, z, y) with x fastest, then z: a half-warp covers one y row pair
+  // (x, z) at fixed y, for which the 40-byte AoS volume stride is conflict-free
+  // (word offsets 4*hz + 5*hx mod 16 are distinct).
+  const int cx = cell % P, cz = (cell / P) % P, cy = cell / (P * P);
   const int warp = tid >> 5, lane = tid & 31;
   constexpr int WPP = C::IVOL >= 32 ? C::IVOL / 32 : 1;   // warps per patch
   const int64_t ngroups = (n_patches + C::PPC - 1) / C::PPC;
@@ -115,11 +129,28 @@ small3d_kernel(const double* __restrict__ qin, double* __restrict__ qout, const 
 
   bool bad = false;
   unsigned stg = 0, par = 0;
+  // per-patch scalars, loaded one iteration ahead (their latency used to stall the closures)
+  auto scalars = [&](int g, double& cs, double& dtp) {
+    cs = 1.0;
+    dtp = 0.0;
+    if (g < G) {
+      const int64_t grp = group_of(g);
+      if (lp < patches_in(grp)) {
+        const int64_t pi = grp * C::PPC + lp;
+        cs = __ldg(cell_size + pi * 3);
+        dtp = __ldg(dtv + pi);
+      }
+    }
+  };
+  double cs_next, dt_next;
+  scalars(0, cs_next, dt_next);
   for (int g = 0; g < G; ++g) {
     const int64_t grp = group_of(g);
     const int np = patches_in(grp);
     const bool active = lp < np;
     const int64_t pidx = grp * C::PPC + lp;
+    const double cs_cur = cs_next, dt_cur = dt_next;
+    scalars(g + 1, cs_next, dt_next);
     const double* st = ring + stg * C::STAGE + lp * C::VOL * S;
     double* side = sideb + lp * C::SIDE;
     mbar_wait(&bars[stg], par);
@@ -133,8 +164,8 @@ small3d_kernel(const double* __restrict__ qin, double* __restrict__ qout, const 
     unsigned long long cmax = 0;
     double inv = 0.0, half_inv = 0.0;
     if (active) {
-      const double dx = __ddiv_rn(cell_size[pidx * 3], (double)P);   // vectorized.py:169
-      inv = __ddiv_rn(dtv[pidx], dx);                                  // vectorized.py:170
+      const double dx = __ddiv_rn(cs_cur, (double)P);   // vectorized.py:169
+      inv = __ddiv_rn(dt_cur, dx);                       // vectorized.py:170
       half_inv = dmul(0.5, inv);
       const unsigned ie = ((unsigned)__double2hiint(inv) >> 20) & 0x7ffu;
       slow = !(inv == 0.0 || (ie >= 2u && ie < 0x7ffu));
@@ -217,7 +248,9 @@ small3d_kernel(const double* __restrict__ qin, double* __restrict__ qout, const 
         }
       }
 #pragma unroll
-      for (int u = 0; u < S; ++u) outb[(g & 1) * C::OUTN + (lp * C::IVOL + cell) * S + u] = val[u];
+      const int lin = (cz * P + cy) * P + cx;   // AoS interior order (x fastest)
+#pragma unroll
+      for (int u = 0; u < S; ++u) outb[(g & 1) * C::OUTN + (lp * C::IVOL + lin) * S + u] = val[u];
       fence_proxy_async();
     }
     // per-patch max wave speed: 64-bit max as (high word, low word) warp reductions
