@@ -34,6 +34,7 @@ extern "C" {
 #define FVB_ERR_CONTRACT 1
 #define FVB_ERR_NONPHYSICAL 2
 #define FVB_ERR_CUDA 3
+#define FVB_ERR_IO 4          /* file open / read / write failure (FVB1 I/O) */
 
 /* kernel selector for fvb_update / fvb_update_host */
 #define FVB_KERNEL_AUTO 0     /* the shape's fused kernel when it has one, else generic */
@@ -142,6 +143,21 @@ int fvb_halo_project(const fvb_spec* spec, const double* qout, double* qin, cons
  * (SPEC.md:446-455, :473).  scratch: fvb_totals_scratch_bytes(spec) bytes. */
 size_t fvb_totals_scratch_bytes(const fvb_spec* spec);
 int fvb_totals(const fvb_spec* spec, const double* qout, double* scratch, double* totals, void* stream);
+
+/* FVB1 batch files (host memory, no device work), byte
+ * compatible with the reference's fixture dumps save_batch / load_batch
+ * (mesh.py:313-353): "FVB1", int64 (d, p, s, N), then QIn, QOut,
+ * cell_centre, cell_size, t, dt, max_eigenvalue as little-endian float64.
+ * fvb_fvb1_header reads the header; fvb_fvb1_read fills caller-sized arrays
+ * (header must equal the file's; a NULL array is skipped);
+ * fvb_fvb1_write writes a dump.  FVB_ERR_CONTRACT on a bad magic / header /
+ * size mismatch, FVB_ERR_IO on file errors. */
+int fvb_fvb1_header(const char* path, int64_t* header /* [4] */);
+int fvb_fvb1_read(const char* path, const int64_t* header, double* qin, double* qout, double* cell_centre,
+                  double* cell_size, double* t, double* dt, double* max_eig);
+int fvb_fvb1_write(const char* path, const int64_t* header, const double* qin, const double* qout,
+                   const double* cell_centre, const double* cell_size, const double* t, const double* dt,
+                   const double* max_eig);
 
 /* Self-test: shared-reciprocal division vs IEEE division for n operand pairs. */
 int fvb_selftest_div(const double* a, const double* b, double* out_shared, double* out_ieee,

@@ -20,6 +20,7 @@ FVB_OK = 0
 FVB_ERR_CONTRACT = 1
 FVB_ERR_NONPHYSICAL = 2
 FVB_ERR_CUDA = 3
+FVB_ERR_IO = 4
 
 KERNEL_AUTO = 0
 KERNEL_GENERIC = 1
@@ -31,6 +32,7 @@ EXPORTED = (
     "fvb_update_host_workspace", "fvb_update_host", "fvb_locate", "fvb_pack", "fvb_unpack",
     "fvb_reduce_dt", "fvb_set_dt", "fvb_patch_max_eig", "fvb_probe", "fvb_selftest_div",
     "fvb_halo_project", "fvb_totals_scratch_bytes", "fvb_totals",
+    "fvb_fvb1_header", "fvb_fvb1_read", "fvb_fvb1_write",
 )
 
 
@@ -91,6 +93,13 @@ def load():
     L.fvb_totals_scratch_bytes.argtypes = [sp]
     L.fvb_totals.restype = i32
     L.fvb_totals.argtypes = [sp, vp, vp, vp, vp]
+    cp, i64p = ctypes.c_char_p, ctypes.POINTER(ctypes.c_int64)
+    L.fvb_fvb1_header.restype = i32
+    L.fvb_fvb1_header.argtypes = [cp, i64p]
+    L.fvb_fvb1_read.restype = i32
+    L.fvb_fvb1_read.argtypes = [cp, i64p] + [vp] * 7
+    L.fvb_fvb1_write.restype = i32
+    L.fvb_fvb1_write.argtypes = [cp, i64p] + [vp] * 7
     L.fvb_selftest_div.restype = i32
     L.fvb_selftest_div.argtypes = [vp, vp, vp, vp, i64, vp]
     _lib = L

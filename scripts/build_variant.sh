@@ -13,6 +13,7 @@ FLAGS="-gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 -fmad=fa
 for f in fvb_capi fvb_generic fvb_fused2d fvb_fused2d_warp fvb_fused3d fvb_fused3d_half fvb_small3d; do
   /usr/local/cuda/bin/nvcc $FLAGS -Xptxas -v -c "$SRC/$f.cu" -o "$B/$f.o" 2> "$B/$f.log" &
 done
+g++ -O2 -fPIC -std=c++17 -c "$SRC/fvb_io.cpp" -o "$B/fvb_io.o" &
 FAIL=0
 for j in $(jobs -p); do wait $j || FAIL=1; done
 if [ $FAIL = 1 ]; then cat "$B"/*.log | grep -i -B2 -A5 error | head -40; rm -rf "$B"; exit 1; fi
