@@ -87,3 +87,41 @@ def test_run_simulation_constant_state_is_fixed_point():
     res = driver.run_simulation(db, grid, steps=10, cfl=0.3, periodic=True)
     assert_bits_equal(db.QOut.cpu().numpy().reshape(n, -1), field, "constant field after 10 steps")
     assert len(set(res.dt)) == 1
+
+
+def _moving_contact(g, p, t):
+    """rho = 1 + 0.2 sin(2 pi (x - t)), u = (1, 0), p = 1 on [0,1]^2, periodic; cell-centre values."""
+    n_ax = g * p
+    xc = (np.arange(n_ax) + 0.5) / n_ax
+    rho = 1.0 + 0.2 * np.sin(2.0 * np.pi * (xc - t))
+    return np.broadcast_to(rho[None, :], (n_ax, n_ax))   # [y, x]
+
+
+def _field_from_global(g, p, glob):
+    """Global [y, x, u] field -> interior QOut rows of a g x g patch grid (patch index x-fastest)."""
+    s = glob.shape[-1]
+    return glob.reshape(g, p, g, p, s).transpose(0, 2, 1, 3, 4).reshape(g * g, p * p * s)
+
+
+def test_run_simulation_convergence_order():
+    """SPEC.md:562 (acceptance criterion 5): moving contact, L1 density error at 30 / 90 / 270
+    volumes per axis decreases with observed order >= 0.7 (first-order Rusanov)."""
+    p, gamma, t_end = 10, 1.4, 0.05
+    errors = []
+    for g in (3, 9, 27):
+        n_ax = g * p
+        rho = _moving_contact(g, p, 0.0)
+        q = np.zeros((n_ax, n_ax, 4))
+        q[..., 0] = rho
+        q[..., 1] = rho * 1.0
+        q[..., 3] = 1.0 / (gamma - 1.0) + 0.5 * rho * 1.0
+        db = _db_with_field(2, p, (g, g), _field_from_global(g, p, q))
+        db.cell_size.fill_(1.0 / g)
+        dx = 1.0 / n_ax
+        steps = int(np.ceil(t_end / (0.4 * dx / (1.0 + np.sqrt(gamma / 0.8)))))
+        res = driver.run_simulation(db, (g, g), steps=steps, cfl=0.4, periodic=True)
+        out = db.QOut.cpu().numpy().reshape(g, g, p, p, 4).transpose(0, 2, 1, 3, 4).reshape(n_ax, n_ax, 4)
+        exact = _moving_contact(g, p, res.t[-1])
+        errors.append(float(np.abs(out[..., 0] - exact).mean()))
+    orders = [np.log(errors[k] / errors[k + 1]) / np.log(3.0) for k in range(2)]
+    assert min(orders) >= 0.7, (errors, orders)
