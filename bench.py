@@ -109,6 +109,38 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
+def pcie_bandwidth(torch, nbytes: int = 256 << 20):
+    """Pinned host <-> device copy bandwidth of this GPU's link (GB/s): H2D alone, D2H alone, and
+    each direction while both run (the e2e pipeline overlaps them).  The e2e roofline."""
+    h = torch.empty(nbytes, dtype=torch.uint8, pin_memory=True)
+    h2 = torch.empty(nbytes, dtype=torch.uint8, pin_memory=True)
+    d = torch.empty(nbytes, dtype=torch.uint8, device="cuda")
+    d2 = torch.empty(nbytes, dtype=torch.uint8, device="cuda")
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+    d.copy_(h, non_blocking=True)
+    h.copy_(d, non_blocking=True)
+    torch.cuda.synchronize()
+
+    def timed(fn, reps=3):
+        t0 = time.perf_counter()
+        for _ in range(reps):
+            fn()
+        torch.cuda.synchronize()
+        return (time.perf_counter() - t0) / reps
+
+    def both():
+        with torch.cuda.stream(s1):
+            d.copy_(h, non_blocking=True)
+        with torch.cuda.stream(s2):
+            h2.copy_(d2, non_blocking=True)
+
+    out = {"h2d": nbytes / timed(lambda: d.copy_(h, non_blocking=True)) / 1e9,
+           "d2h": nbytes / timed(lambda: h.copy_(d, non_blocking=True)) / 1e9,
+           "bidir_each": nbytes / timed(both) / 1e9}
+    del h, h2, d, d2
+    return out
+
+
 def cpu_cores() -> int:
     try:
         return len(os.sched_getaffinity(0))
@@ -313,10 +345,19 @@ def main():
             t = torch.tensor([e2e_ms], dtype=torch.float64, device="cuda")
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             e2e_ms = float(t[0])
+        h2d_b = int(host.QIn.nbytes + host.cell_size.nbytes + host.dt.nbytes)
+        d2h_b = int(host.QOut.nbytes + host.max_eigenvalue.nbytes)
         e2e = {"value": world * cells_per_gpu * args.e2e_steps / (e2e_ms * 1e-3), "unit": "cell updates/s",
-               "h2d_bytes_per_step": int(host.QIn.nbytes + host.cell_size.nbytes + host.dt.nbytes),
-               "d2h_bytes_per_step": int(host.QOut.nbytes + host.max_eigenvalue.nbytes),
+               "h2d_bytes_per_step": h2d_b, "d2h_bytes_per_step": d2h_b,
                "steps": args.e2e_steps, "path": "kernel.update_patch_batch (pinned numpy in, numpy out)"}
+        # e2e roofline: the PCIe link, both directions busy at once (copies of chunk k+1 in,
+        # chunk k-1 out overlap the kernel of chunk k in fvb_update_host)
+        bw = pcie_bandwidth(torch)
+        t_bound = max(h2d_b / (bw["bidir_each"] * 1e9), d2h_b / (bw["bidir_each"] * 1e9),
+                      h2d_b / (bw["h2d"] * 1e9) + 0.0, (h2d_b + d2h_b) / ((bw["h2d"] + bw["d2h"]) * 1e9))
+        bound = world * cells_per_gpu / t_bound
+        e2e["pcie_gbs"] = {k: round(v, 2) for k, v in bw.items()}
+        e2e["roofline"] = {"bound": "pcie", "value": bound, "frac": e2e["value"] / bound}
         del host
 
     cpu = None
