@@ -353,8 +353,8 @@ def main():
         # e2e roofline: the PCIe link, both directions busy at once (copies of chunk k+1 in,
         # chunk k-1 out overlap the kernel of chunk k in fvb_update_host)
         bw = pcie_bandwidth(torch)
-        t_bound = max(h2d_b / (bw["bidir_each"] * 1e9), d2h_b / (bw["bidir_each"] * 1e9),
-                      h2d_b / (bw["h2d"] * 1e9) + 0.0, (h2d_b + d2h_b) / ((bw["h2d"] + bw["d2h"]) * 1e9))
+        t_bound = max(h2d_b / (bw["h2d"] * 1e9), d2h_b / (bw["d2h"] * 1e9),
+                      (h2d_b + d2h_b) / (2.0 * bw["bidir_each"] * 1e9))
         bound = world * cells_per_gpu / t_bound
         e2e["pcie_gbs"] = {k: round(v, 2) for k, v in bw.items()}
         e2e["roofline"] = {"bound": "pcie", "value": bound, "frac": e2e["value"] / bound}
