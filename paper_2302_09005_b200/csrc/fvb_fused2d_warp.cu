@@ -51,8 +51,8 @@ constexpr int HXR = 8;                    // halo x-side ring rows
 constexpr int HXC = HXR * 4;              // halo x-side doubles per component: [row slot][side][patch slot]
 constexpr int HXS = 4 * HXC;              // [c][row slot][side][patch slot]
 constexpr int OUTR = P * S;               // one output row of one patch (512 B)
-constexpr int OFFO = 66;                  // patch-B output offset: 528 B = 16 mod 128
-constexpr int OUTD = 136;                 // output staging per row parity
+constexpr int OFFO = 130;                 // patch-B output offset: 1,040 B = 16 mod 128
+constexpr int OUTD = OFFO + 2 * OUTR;     // output staging: two rows of each patch, stored together
 constexpr int WPC = 4;                    // warps per CTA
 #ifndef FVB2D_HY_UNROLL
 #define FVB2D_HY_UNROLL 2
@@ -62,7 +62,7 @@ constexpr int W_RING = 0;
 constexpr int W_XS = W_RING + NS * STGD;
 constexpr int W_HX = W_XS + 2 * XSD;
 constexpr int W_OUT = W_HX + HXS;
-constexpr int W_BAR = W_OUT + 2 * OUTD;
+constexpr int W_BAR = W_OUT + OUTD;
 constexpr int WARPD = (W_BAR + NS + 1) & ~1;   // doubles per warp (16 B multiple)
 constexpr size_t BYTES = (size_t)WPC * WARPD * 8;
 
@@ -310,18 +310,23 @@ fused2d_warp_kernel(const double* __restrict__ qin, double* __restrict__ qout, c
             if (is_negzero(val[u]) && is_negzero(qlow)) val[u] = 0.0;
           }
         }
-        // stage the output row; the buffer of this parity was last stored two rows ago
-        if (l == 0) bulk_wait_read<1>();
-        __syncwarp();
-        double* ob = outb + (hy & 1) * OUTD;
-        sts_q(ob + ps * OFFO + x * S, val);
-        fence_proxy_async();
-        __syncwarp();
-        if (l == 0) {
-          const int z = hy - 2;
-          tma_store_1d(qout + (pa * IVOL + z * P) * S, ob, (uint32_t)(OUTR * 8));
-          if (pa + 1 < n) tma_store_1d(qout + ((pa + 1) * IVOL + z * P) * S, ob + OFFO, (uint32_t)(OUTR * 8));
-          bulk_commit();
+        // stage the output row; rows are stored in pairs (one 1 KB bulk store per patch), so
+        // before the first row of a pair the previous pair's store must have read the buffer
+        const int z = hy - 2;
+        if (!(z & 1)) {
+          if (l == 0) bulk_wait_read<0>();
+          __syncwarp();
+        }
+        sts_q(outb + ps * OFFO + (z & 1) * OUTR + x * S, val);
+        if (z & 1) {
+          fence_proxy_async();
+          __syncwarp();
+          if (l == 0) {
+            tma_store_1d(qout + (pa * IVOL + (z - 1) * P) * S, outb, (uint32_t)(2 * OUTR * 8));
+            if (pa + 1 < n)
+              tma_store_1d(qout + ((pa + 1) * IVOL + (z - 1) * P) * S, outb + OFFO, (uint32_t)(2 * OUTR * 8));
+            bulk_commit();
+          }
         }
       }
       if (done >= 1) {
