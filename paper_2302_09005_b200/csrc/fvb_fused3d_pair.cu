@@ -25,7 +25,11 @@ namespace f3p {
 using namespace f16;
 
 constexpr int P = 16, E = 18, S = 5;
-constexpr int R = 8;                      // interior rows per half
+#ifndef FVB3D_PAIR_ROWS
+#define FVB3D_PAIR_ROWS 8
+#endif
+constexpr int R = FVB3D_PAIR_ROWS;        // interior rows per CTA work item (8: half patches, 16: whole patches)
+constexpr int IPP = P / R;                // work items per patch
 constexpr int SR = R + 2;                 // stage rows (halo/ghost above and below)
 constexpr int PLANE = E * E;
 constexpr int SVOL = SR * E;
@@ -37,14 +41,14 @@ constexpr int64_t IVOL = (int64_t)P * P * P;
 constexpr int YS = S * SR * P;            // ys: [c][stage row 0..9][x 0..15]
 constexpr int XS = S * R * E;             // xs: [c][local row 0..7][hx 0..17]
 constexpr int OUTN = R * P * S;
-constexpr int NIW = 2;                    // interior warps
+constexpr int NIW = R / 4;                // interior warps (a warp covers 2 row pairs)
 constexpr int NTHREADS = 32 * (NIW + 1);
 constexpr int OFF_RING = 0;
 constexpr int OFF_YS = OFF_RING + NST * STAGE;
 constexpr int OFF_XS = OFF_YS + 2 * YS;
 constexpr int OFF_OUT = OFF_XS + 2 * XS;
 constexpr int OFF_WMAX = OFF_OUT + 2 * OUTN;
-constexpr int OFF_FLAG = OFF_WMAX + 4;
+constexpr int OFF_FLAG = OFF_WMAX + 2 * NIW;
 constexpr int OFF_BAR = OFF_FLAG + 1;
 constexpr int TOTAL = OFF_BAR + NST;
 constexpr size_t BYTES = (size_t)TOTAL * 8;
@@ -99,7 +103,7 @@ template <int K>
 using Kind = std::integral_constant<int, K>;
 
 template <int L>
-__global__ void __launch_bounds__(NTHREADS, 4)
+__global__ void __launch_bounds__(NTHREADS, R == 8 ? 4 : 2)
 fused3d_pair_kernel(const double* __restrict__ qin, double* __restrict__ qout, const double* __restrict__ cell_size,
                     const double* __restrict__ dtv, double* __restrict__ max_eig, unsigned* __restrict__ status,
                     int64_t n, Closure cl) {
@@ -116,17 +120,17 @@ fused3d_pair_kernel(const double* __restrict__ qin, double* __restrict__ qout, c
   const bool interior = tid < 32 * NIW;
   const int warp = tid >> 5, lane = tid & 31;
   const int x = lane & 15;
-  const int lya = (((warp & 1) << 1) | (lane >> 4)) * 2;   // local rows lya, lya + 1
+  const int lya = ((warp << 1) | (lane >> 4)) * 2;   // local rows lya, lya + 1 (interior warps)
   const bool producer = tid == 32 * NIW;
 
-  const int64_t items = 2 * n;
+  const int64_t items = IPP * n;
   const int my_items = (items > (int64_t)blockIdx.x) ? (int)((items - 1 - (int64_t)blockIdx.x) / gridDim.x + 1) : 0;
   auto item_index = [&](int j) -> int64_t { return (int64_t)blockIdx.x + (int64_t)j * gridDim.x; };
 
   auto issue = [&](int j, int zh, unsigned s) {
     const int64_t it = item_index(j);
-    const int64_t pidx = it >> 1;
-    const int y0 = (int)(it & 1) * R;
+    const int64_t pidx = it / IPP;
+    const int y0 = (int)(it % IPP) * R;
     double* st = ring + s * STAGE;
     uint64_t* bar = bars + s;
     fence_proxy_async();
@@ -153,9 +157,12 @@ fused3d_pair_kernel(const double* __restrict__ qin, double* __restrict__ qout, c
     bulk_commit();
   };
   auto finish_item = [&](int j, int64_t pidx) {
-    unsigned long long m = wmax[(j & 1) * 2];
-    const unsigned long long v = wmax[(j & 1) * 2 + 1];
-    m = v > m ? v : m;
+    unsigned long long m = wmax[(j & 1) * NIW];
+#pragma unroll
+    for (int w = 1; w < NIW; ++w) {
+      const unsigned long long v = wmax[(j & 1) * NIW + w];
+      m = v > m ? v : m;
+    }
     atomicMax(reinterpret_cast<unsigned long long*>(max_eig) + pidx, m);
     if (slowflag[j & 1]) {
       const unsigned k = atomicAdd(&status[1], 1u);
@@ -190,8 +197,8 @@ fused3d_pair_kernel(const double* __restrict__ qin, double* __restrict__ qout, c
 
   for (int jp = 0; jp < my_items; ++jp) {
     const int64_t it = item_index(jp);
-    const int64_t pidx = it >> 1;
-    const int y0 = (int)(it & 1) * R;
+    const int64_t pidx = it / IPP;
+    const int y0 = (int)(it % IPP) * R;
     const double dx = __ddiv_rn(cell_size[pidx * 3], (double)P);   // vectorized.py:169
     const double inv = __ddiv_rn(dtv[pidx], dx);                    // vectorized.py:170
     const double half_inv = dmul(0.5, inv);
@@ -367,9 +374,9 @@ fused3d_pair_kernel(const double* __restrict__ qin, double* __restrict__ qout, c
           slow = slow | !ok;
           put_ys(ys_w, r, x, sh);
         }
-        if (lane < 16) {
-          const int lr = lane & 7;
-          const int hx = lane < 8 ? 0 : E - 1;
+        if (lane < 2 * R) {
+          const int lr = lane % R;
+          const int hx = lane < R ? 0 : E - 1;
           double qh[S];
           load_q<L>(st, lr + 1, hx, qh);
           Side<3> sh;
@@ -390,7 +397,7 @@ fused3d_pair_kernel(const double* __restrict__ qin, double* __restrict__ qout, c
             const unsigned long long v = __shfl_xor_sync(0xffffffffu, m, o);
             m = v > m ? v : m;
           }
-          if (lane == 0) wmax[(jp & 1) * 2 + warp] = m;
+          if (lane == 0) wmax[(jp & 1) * NIW + warp] = m;
           cm = 0;
         }
       }
@@ -433,7 +440,7 @@ cudaError_t launch_impl(const FvbArgs& a, cudaStream_t st) {
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kfn, NTHREADS, BYTES);
   if (per_sm < 1) per_sm = 1;
   int64_t grid = (int64_t)sms * per_sm;
-  if (grid > 2 * a.n) grid = 2 * a.n;
+  if (grid > IPP * a.n) grid = IPP * a.n;
   const Closure cl{a.gamma, a.gamma - 1.0};
   kfn<<<(unsigned)grid, NTHREADS, BYTES, st>>>(a.qin, a.qout, a.cell_size, a.dt, a.max_eig, a.status, a.n, cl);
   return cudaGetLastError();
