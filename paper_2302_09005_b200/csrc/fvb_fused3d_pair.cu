@@ -41,7 +41,11 @@ constexpr int64_t IVOL = (int64_t)P * P * P;
 constexpr int YS = S * SR * P;            // ys: [c][stage row 0..9][x 0..15]
 constexpr int XS = S * R * E;             // xs: [c][local row 0..7][hx 0..17]
 constexpr int OUTN = R * P * S;
-constexpr int NIW = R / 4;                // interior warps (a warp covers 2 row pairs)
+#ifndef FVB3D_PAIR_CELLS
+#define FVB3D_PAIR_CELLS 2
+#endif
+constexpr int KC = FVB3D_PAIR_CELLS;      // cells per thread along y (2 or 4)
+constexpr int NIW = R / (2 * KC);         // interior warps (a warp covers 2 row groups of KC rows)
 constexpr int NTHREADS = 32 * (NIW + 1);
 constexpr int OFF_RING = 0;
 constexpr int OFF_YS = OFF_RING + NST * STAGE;
@@ -103,7 +107,7 @@ template <int K>
 using Kind = std::integral_constant<int, K>;
 
 template <int L>
-__global__ void __launch_bounds__(NTHREADS, R == 8 ? 4 : 2)
+__global__ void __launch_bounds__(NTHREADS, (R == 8 && KC == 2) ? 4 : (R == 8 ? 4 : 2))
 fused3d_pair_kernel(const double* __restrict__ qin, double* __restrict__ qout, const double* __restrict__ cell_size,
                     const double* __restrict__ dtv, double* __restrict__ max_eig, unsigned* __restrict__ status,
                     int64_t n, Closure cl) {
@@ -120,7 +124,7 @@ fused3d_pair_kernel(const double* __restrict__ qin, double* __restrict__ qout, c
   const bool interior = tid < 32 * NIW;
   const int warp = tid >> 5, lane = tid & 31;
   const int x = lane & 15;
-  const int lya = ((warp << 1) | (lane >> 4)) * 2;   // local rows lya, lya + 1 (interior warps)
+  const int lya = ((warp << 1) | (lane >> 4)) * KC;   // local rows lya .. lya + KC - 1 (interior warps)
   const bool producer = tid == 32 * NIW;
 
   const int64_t items = IPP * n;
@@ -186,12 +190,15 @@ fused3d_pair_kernel(const double* __restrict__ qin, double* __restrict__ qout, c
   bool bad = false;
   bool slow = false;
   unsigned long long cm = 0;
-  ZCarry za, zb;
+  ZCarry zk[KC];
 #pragma unroll
-  for (int u = 0; u < S; ++u) { za.tp[u] = za.favg[u] = zb.tp[u] = zb.favg[u] = 0.0; }
-  za.prev.lam = zb.prev.lam = 0.0;
+  for (int c = 0; c < KC; ++c) {
 #pragma unroll
-  for (int k = 0; k < 4; ++k) za.prev.f[k] = zb.prev.f[k] = 0.0;
+    for (int u = 0; u < S; ++u) { zk[c].tp[u] = 0.0; zk[c].favg[u] = 0.0; }
+    zk[c].prev.lam = 0.0;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) zk[c].prev.f[k] = 0.0;
+  }
 
   unsigned stg = 0, par = 0;
 
@@ -215,11 +222,6 @@ fused3d_pair_kernel(const double* __restrict__ qin, double* __restrict__ qout, c
       mbar_wait(&bars[stg], par);
 
       if (interior) {
-        // ---- A: closures of this thread's two volumes of plane zh ----
-        Side<3> zca, zcb;
-        double qa[S], qb[S];
-        load_q<L>(st, lya + 1, x + 1, qa);
-        load_q<L>(st, lya + 2, x + 1, qb);
         auto closure = [&](const double (&q)[S], int ly, Side<3>& zc) {
           if (K == kFirst || K == kSteady) {
             Side<3> sd[3];
@@ -243,123 +245,116 @@ fused3d_pair_kernel(const double* __restrict__ qin, double* __restrict__ qout, c
             slow = slow | !ok;
           }
         };
-        closure(qa, lya, zca);
-        closure(qb, lya + 1, zcb);
-        if (K == kFirst) {
-          auto first_face = [&](const double (&q)[S], int ly, const Side<3>& zc, ZCarry& zz) {
-            double qc[S];
-            load_q<L>(stc, ly + 1, x + 1, qc);
-            const double cz = dmul(half_inv, speed_max(zc.lam, zz.prev.lam));
+        auto first_face = [&](const double (&q)[S], int ly, const Side<3>& zc, ZCarry& zz) {
+          double qc[S];
+          load_q<L>(stc, ly + 1, x + 1, qc);
+          const double cz = dmul(half_inv, speed_max(zc.lam, zz.prev.lam));
+#pragma unroll
+          for (int u = 0; u < S; ++u) {
+            zz.tp[u] = dmul(cz, dsub(q[u], qc[u]));
+            const double c = u == 0 ? qc[3] : zz.prev.f[u - 1];
+            zz.favg[u] = dadd(c, u == 0 ? q[3] : zc.f[u - 1]);
+          }
+        };
+        // y neighbour record (state, y wave speed, y fluxes) of stage row r, plane zh-1
+        auto load_ynb = [&](int r, YNb& o) {
+          load_q<L>(stc, r, x + 1, o.q);
+          o.lam = ys_r[ys_at(0, r, x)];
+#pragma unroll
+          for (int k = 0; k < 4; ++k) o.f[k] = ys_r[ys_at(k + 1, r, x)];
+        };
+        // update of the cell at local row ly of plane zh-1 (vectorized.py:161-200)
+        auto update = [&](const YNb& own, const YNb& ym, const YNb& yp, int ly, const double (&q)[S],
+                          const Side<3>& zc, ZCarry& zz) {
+          double val[S], qn[S];
+          const double lx = xs_r[xs_at(0, ly, x + 1)];
+          const double cz = dmul(half_inv, speed_max(zc.lam, zz.prev.lam));
+#pragma unroll
+          for (int u = 0; u < S; ++u) val[u] = own.q[u];                      // _pass_copy
+          // dissipation x-, x+, y-, y+ (vectorized.py:173-180)
+          load_q<L>(stc, ly + 1, x, qn);
+          const double jl = qn[1];
+          dissipate<3>(val, half_inv, lx, own.q, xs_r[xs_at(0, ly, x)], qn);
+          load_q<L>(stc, ly + 1, x + 2, qn);
+          const double jr = qn[1];
+          dissipate<3>(val, half_inv, lx, own.q, xs_r[xs_at(0, ly, x + 2)], qn);
+          dissipate<3>(val, half_inv, own.lam, own.q, ym.lam, ym.q);
+          dissipate<3>(val, half_inv, own.lam, own.q, yp.lam, yp.q);
+          // z-: the previous face's term, negated; z+: this face's term
+#pragma unroll
+          for (int u = 0; u < S; ++u) val[u] = dsub(val[u], zz.tp[u]);
+#pragma unroll
+          for (int u = 0; u < S; ++u) {
+            zz.tp[u] = dmul(cz, dsub(q[u], own.q[u]));
+            val[u] = dadd(val[u], zz.tp[u]);
+          }
+          // flux differences x, y, z (vectorized.py:193-200), see fvb_fused3d.cu add_flux
+#pragma unroll
+          for (int u = 0; u < S; ++u) {
+            const double fm = u == 0 ? jl : xs_r[xs_at(u, ly, x)];
+            const double fc = u == 0 ? own.q[1] : xs_r[xs_at(u, ly, x + 1)];
+            const double fp = u == 0 ? jr : xs_r[xs_at(u, ly, x + 2)];
+            val[u] = dadd(val[u], dmul(half_inv, dsub(dadd(fm, fc), dadd(fc, fp))));
+          }
+#pragma unroll
+          for (int u = 0; u < S; ++u) {
+            const double fm = u == 0 ? ym.q[2] : ym.f[u - 1];
+            const double fc = u == 0 ? own.q[2] : own.f[u - 1];
+            const double fp = u == 0 ? yp.q[2] : yp.f[u - 1];
+            val[u] = dadd(val[u], dmul(half_inv, dsub(dadd(fm, fc), dadd(fc, fp))));
+          }
+#pragma unroll
+          for (int u = 0; u < S; ++u) {
+            const double c = u == 0 ? own.q[3] : zz.prev.f[u - 1];
+            const double sum_p = dadd(c, u == 0 ? q[3] : zc.f[u - 1]);
+            val[u] = dadd(val[u], dmul(half_inv, dsub(zz.favg[u], sum_p)));
+            zz.favg[u] = sum_p;
+          }
+          // fix_negzero (fvb_fused3d.cu)
+          bool nz = false;
+#pragma unroll
+          for (int u = 0; u < S; ++u) nz = nz | is_negzero(val[u]);
+          if (__builtin_expect(nz, 0)) {
+            const int64_t vlow = ((int64_t)(zh - 2) * E + (y0 + ly + 1)) * E + (x + 1);
 #pragma unroll
             for (int u = 0; u < S; ++u) {
-              zz.tp[u] = dmul(cz, dsub(q[u], qc[u]));
-              const double c = u == 0 ? qc[3] : zz.prev.f[u - 1];
-              zz.favg[u] = dadd(c, u == 0 ? q[3] : zc.f[u - 1]);
+              const double qlow =
+                  L == kAoS ? qin[(pidx * VOL + vlow) * S + u] : qin[((int64_t)u * n + pidx) * VOL + vlow];
+              if (is_negzero(val[u]) && is_negzero(qlow)) val[u] = 0.0;
             }
-          };
-          first_face(qa, lya, zca, za);
-          first_face(qb, lya + 1, zcb, zb);
-        }
+          }
+          double* ob_ = outb + (zh & 1) * OUTN;
+#pragma unroll
+          for (int u = 0; u < S; ++u) {
+            if (L == kAoS) ob_[(ly * P + x) * S + u] = val[u];
+            else ob_[(u * R + ly) * P + x] = val[u];
+          }
+        };
+        // Cell by cell along y: closure of the cell's volume of plane zh, then its
+        // update of plane zh-1 through a sliding window of three y-neighbour
+        // records (the cells of a group are each other's y neighbours).
+        YNb wm, wc, wp;
         if (K == kSteady || K == kZHi) {
-          // ---- B: updates of this thread's two cells of plane zh-1 ----
-          // own data of both cells (each is also the other's y neighbour)
-          YNb oa, ob;
-          load_q<L>(stc, lya + 1, x + 1, oa.q);
-          load_q<L>(stc, lya + 2, x + 1, ob.q);
-          oa.lam = ys_r[ys_at(0, lya + 1, x)];
-          ob.lam = ys_r[ys_at(0, lya + 2, x)];
-#pragma unroll
-          for (int k = 0; k < 4; ++k) {
-            oa.f[k] = ys_r[ys_at(k + 1, lya + 1, x)];
-            ob.f[k] = ys_r[ys_at(k + 1, lya + 2, x)];
-          }
-          auto update = [&](const YNb& own, const YNb& ym, const YNb& yp, int ly, const double (&q)[S],
-                            const Side<3>& zc, ZCarry& zz, int half) {
-            double val[S], qn[S];
-            const double lx = xs_r[xs_at(0, ly, x + 1)];
-            const double cz = dmul(half_inv, speed_max(zc.lam, zz.prev.lam));
-#pragma unroll
-            for (int u = 0; u < S; ++u) val[u] = own.q[u];                      // _pass_copy
-            // dissipation x-, x+, y-, y+ (vectorized.py:173-180)
-            load_q<L>(stc, ly + 1, x, qn);
-            const double jl = qn[1];
-            dissipate<3>(val, half_inv, lx, own.q, xs_r[xs_at(0, ly, x)], qn);
-            load_q<L>(stc, ly + 1, x + 2, qn);
-            const double jr = qn[1];
-            dissipate<3>(val, half_inv, lx, own.q, xs_r[xs_at(0, ly, x + 2)], qn);
-            dissipate<3>(val, half_inv, own.lam, own.q, ym.lam, ym.q);
-            dissipate<3>(val, half_inv, own.lam, own.q, yp.lam, yp.q);
-            // z-: the previous face's term, negated; z+: this face's term
-#pragma unroll
-            for (int u = 0; u < S; ++u) val[u] = dsub(val[u], zz.tp[u]);
-#pragma unroll
-            for (int u = 0; u < S; ++u) {
-              zz.tp[u] = dmul(cz, dsub(q[u], own.q[u]));
-              val[u] = dadd(val[u], zz.tp[u]);
-            }
-            // flux differences x, y, z (vectorized.py:193-200), see fvb_fused3d.cu add_flux
-#pragma unroll
-            for (int u = 0; u < S; ++u) {
-              const double fm = u == 0 ? jl : xs_r[xs_at(u, ly, x)];
-              const double fc = u == 0 ? own.q[1] : xs_r[xs_at(u, ly, x + 1)];
-              const double fp = u == 0 ? jr : xs_r[xs_at(u, ly, x + 2)];
-              val[u] = dadd(val[u], dmul(half_inv, dsub(dadd(fm, fc), dadd(fc, fp))));
-            }
-#pragma unroll
-            for (int u = 0; u < S; ++u) {
-              const double fm = u == 0 ? ym.q[2] : ym.f[u - 1];
-              const double fc = u == 0 ? own.q[2] : own.f[u - 1];
-              const double fp = u == 0 ? yp.q[2] : yp.f[u - 1];
-              val[u] = dadd(val[u], dmul(half_inv, dsub(dadd(fm, fc), dadd(fc, fp))));
-            }
-#pragma unroll
-            for (int u = 0; u < S; ++u) {
-              const double c = u == 0 ? own.q[3] : zz.prev.f[u - 1];
-              const double sum_p = dadd(c, u == 0 ? q[3] : zc.f[u - 1]);
-              val[u] = dadd(val[u], dmul(half_inv, dsub(zz.favg[u], sum_p)));
-              zz.favg[u] = sum_p;
-            }
-            // fix_negzero (fvb_fused3d.cu)
-            bool nz = false;
-#pragma unroll
-            for (int u = 0; u < S; ++u) nz = nz | is_negzero(val[u]);
-            if (__builtin_expect(nz, 0)) {
-              const int64_t vlow = ((int64_t)(zh - 2) * E + (y0 + ly + 1)) * E + (x + 1);
-#pragma unroll
-              for (int u = 0; u < S; ++u) {
-                const double qlow =
-                    L == kAoS ? qin[(pidx * VOL + vlow) * S + u] : qin[((int64_t)u * n + pidx) * VOL + vlow];
-                if (is_negzero(val[u]) && is_negzero(qlow)) val[u] = 0.0;
-              }
-            }
-            double* ob_ = outb + (zh & 1) * OUTN;
-#pragma unroll
-            for (int u = 0; u < S; ++u) {
-              if (L == kAoS) ob_[(ly * P + x) * S + u] = val[u];
-              else ob_[(u * R + ly) * P + x] = val[u];
-            }
-            (void)half;
-          };
-          {   // cell A: y- neighbour from shared memory, y+ neighbour is B
-            YNb ym;
-            load_q<L>(stc, lya, x + 1, ym.q);
-            ym.lam = ys_r[ys_at(0, lya, x)];
-#pragma unroll
-            for (int k = 0; k < 4; ++k) ym.f[k] = ys_r[ys_at(k + 1, lya, x)];
-            update(oa, ym, ob, lya, qa, zca, za, 0);
-          }
-          {   // cell B: y- neighbour is A, y+ neighbour from shared memory
-            YNb yp;
-            load_q<L>(stc, lya + 3, x + 1, yp.q);
-            yp.lam = ys_r[ys_at(0, lya + 3, x)];
-#pragma unroll
-            for (int k = 0; k < 4; ++k) yp.f[k] = ys_r[ys_at(k + 1, lya + 3, x)];
-            update(ob, oa, yp, lya + 1, qb, zcb, zb, 1);
-          }
-          fence_proxy_async();
+          load_ynb(lya, wm);       // y- neighbour of the first cell (shared memory)
+          load_ynb(lya + 1, wc);   // the first cell itself
         }
-        za.prev = zca;
-        zb.prev = zcb;
+#pragma unroll
+        for (int c = 0; c < KC; ++c) {
+          const int ly = lya + c;
+          double q[S];
+          Side<3> zc;
+          load_q<L>(st, ly + 1, x + 1, q);
+          closure(q, ly, zc);
+          if (K == kFirst) first_face(q, ly, zc, zk[c]);
+          if (K == kSteady || K == kZHi) {
+            load_ynb(ly + 2, wp);   // next cell of the group, or the y+ neighbour after the last
+            update(wc, wm, wp, ly, q, zc, zk[c]);
+            wm = wc;
+            wc = wp;
+          }
+          zk[c].prev = zc;
+        }
+        if (K == kSteady || K == kZHi) fence_proxy_async();
       } else if (K == kFirst || K == kSteady) {
         // the halo warp: stage rows 0 and 9 (y-face halo row and ghost row: y-side data);
         // the x-face halo columns of the 8 interior rows (x-side data)
