@@ -162,7 +162,6 @@ fused2d_kernel(const double* __restrict__ qin, double* __restrict__ qout, const 
   if (producer)
     for (int g = 0; g < NST - 1 && g < G; ++g) issue(g);
 
-  bool bad = false;
   unsigned long long cmax = 0;            // this lane's wave speed of the patch in flight
   unsigned stg = 0, par = 0, slot3 = 0;   // ring stage / mbarrier parity / g % 3 of patch g
   // Software pipeline, ONE CTA barrier per patch: iteration g evaluates the
@@ -181,8 +180,7 @@ fused2d_kernel(const double* __restrict__ qin, double* __restrict__ qout, const 
       load_q<L>(st, y + 1, x + 1, q);
       Side<2> sd[2];
       bool ok;
-      const Thermo<2> T = closure_all_ranged<2>(q, cl, sd, ok);
-      bad = bad | (ok & T.bad);
+      closure_all_ranged<2>(q, cl, sd, ok);
       slow = slow | !ok;
       const unsigned long long a = (unsigned long long)__double_as_longlong(sd[0].lam);
       const unsigned long long b = (unsigned long long)__double_as_longlong(sd[1].lam);
@@ -266,8 +264,7 @@ fused2d_kernel(const double* __restrict__ qin, double* __restrict__ qout, const 
         load_q<L>(st, hy, x + 1, q);
         Side<2> sh;
         bool ok;
-        const Thermo<2> T = closure_one_ranged<2>(q, cl, 1, sh, ok);
-        bad = bad | (ok & T.bad);
+        closure_one_ranged<2>(q, cl, 1, sh, ok);
         slow = slow | !ok;
         put_ys(ys_w, hy, x, sh);
       }
@@ -277,8 +274,7 @@ fused2d_kernel(const double* __restrict__ qin, double* __restrict__ qout, const 
         load_q<L>(st, x + 1, hx, q);
         Side<2> sh;
         bool ok;
-        const Thermo<2> T = closure_one_ranged<2>(q, cl, 0, sh, ok);
-        bad = bad | (ok & T.bad);
+        closure_one_ranged<2>(q, cl, 0, sh, ok);
         slow = slow | !ok;
         put_xs(xs_w, x, hx, sh);
       }
@@ -300,9 +296,7 @@ fused2d_kernel(const double* __restrict__ qin, double* __restrict__ qout, const 
     slot3 = slot3 == 2 ? 0 : slot3 + 1;
   }
 
-  const int any_bad = __syncthreads_or(bad ? 1 : 0);
   if (producer) bulk_wait_all0();
-  if (tid == 0 && any_bad) atomicOr(status, 1u);
 }
 
 template <int L>

@@ -24,7 +24,7 @@
 //
 // Arithmetic: the reference's operation order, bit for bit (fvb_exact.cuh);
 // the re-used y face differs from the reference only in the sign of an exact
-// zero, repaired exactly as in fvb_fused3d.cu (fix_negzero).  AoS only (the
+// zero, which cannot occur inside the range gate (see fvb_fused3d.cu).  AoS only (the
 // packed SoA layout uses the block kernel).
 #include <cuda_runtime.h>
 
@@ -78,9 +78,6 @@ __device__ __forceinline__ void sts_q(double* p, const double (&q)[S]) {
 __device__ __forceinline__ bool inv_ok(double inv) {
   const unsigned e = ((unsigned)__double2hiint(inv) >> 20) & 0x7ffu;
   return inv == 0.0 || (e >= 2u && e < 0x7ffu);
-}
-__device__ __forceinline__ bool is_negzero(double v) {
-  return (unsigned long long)__double_as_longlong(v) == 0x8000000000000000ull;
 }
 
 __global__ void __launch_bounds__(WPC * 32, 4)
@@ -141,7 +138,6 @@ fused2d_warp_kernel(const double* __restrict__ qin, double* __restrict__ qout, c
   const bool lh = x == 0, rh = x == P - 1;          // neighbour is a face-halo column
   const int lcs = lh ? HXC : 32, rcs = rh ? HXC : 32;   // component strides of the neighbours' x-side data
 
-  bool bad = false;
   int s = 0;          // ring stage of the current row
   unsigned par = 0;   // its mbarrier phase parity
   int done = 0;       // rows consumed (refill trigger)
@@ -204,9 +200,7 @@ fused2d_warp_kernel(const double* __restrict__ qin, double* __restrict__ qout, c
           lds_q(hst + (side ? E - 1 : 0) * S, qh);
           Side<2> sh;
           bool ok;
-          const Thermo<2> T = closure_one_ranged<2>(qh, cl, 0, sh, ok);
-          const bool hv = pa + hps < n;
-          bad = bad | (hv & ok & T.bad);
+          closure_one_ranged<2>(qh, cl, 0, sh, ok);
           const int idx = (((hy + dr - 1) & (HXR - 1)) * 2 + side) * 2 + hps;
           hxs[0 * HXC + idx] = sh.lam;
 #pragma unroll
@@ -226,8 +220,7 @@ fused2d_warp_kernel(const double* __restrict__ qin, double* __restrict__ qout, c
       if (hy >= 1 && hy <= P) {
         Side<2> sd2[2];
         bool ok;
-        const Thermo<2> T = closure_all_ranged<2>(q, cl, sd2, ok);
-        bad = bad | (valid & ok & T.bad);
+        closure_all_ranged<2>(q, cl, sd2, ok);
         slow = slow | !ok;
         const unsigned long long a = (unsigned long long)__double_as_longlong(sd2[0].lam);
         const unsigned long long b = (unsigned long long)__double_as_longlong(sd2[1].lam);
@@ -243,8 +236,7 @@ fused2d_warp_kernel(const double* __restrict__ qin, double* __restrict__ qout, c
         ycur = sd2[1];
       } else {   // y-face halo rows: only their y-side data
         bool ok;
-        const Thermo<2> T = closure_one_ranged<2>(q, cl, 1, ycur, ok);
-        bad = bad | (valid & ok & T.bad);
+        closure_one_ranged<2>(q, cl, 1, ycur, ok);
         slow = slow | !ok;
       }
       __syncwarp();   // x-side row hy and the halo batch are visible to the warp
@@ -298,18 +290,6 @@ fused2d_warp_kernel(const double* __restrict__ qin, double* __restrict__ qout, c
           val[u] = dadd(val[u], dmul(half_inv, dsub(favg[u], sum_p)));
           favg[u] = sum_p;
         }
-        // fix_negzero (fvb_fused3d.cu): a -0.0 result whose lower neighbour
-        // holds -0.0 in that unknown is +0.0 in the reference
-        bool nz = false;
-#pragma unroll
-        for (int u = 0; u < S; ++u) nz = nz | is_negzero(val[u]);
-        if (__builtin_expect(nz, 0)) {
-#pragma unroll
-          for (int u = 0; u < S; ++u) {
-            const double qlow = qin[(pl * VOL + (int64_t)(hy - 2) * E + (x + 1)) * S + u];
-            if (is_negzero(val[u]) && is_negzero(qlow)) val[u] = 0.0;
-          }
-        }
         // stage the output row; rows are stored in pairs (one 1 KB bulk store per patch), so
         // before the first row of a pair the previous pair's store must have read the buffer
         const int z = hy - 2;
@@ -360,7 +340,6 @@ fused2d_warp_kernel(const double* __restrict__ qin, double* __restrict__ qout, c
     }
   }
   if (l == 0) bulk_wait_all0();
-  if (__any_sync(0xffffffffu, bad) && l == 0) atomicOr(status, 1u);
 }
 
 }  // namespace f2w

@@ -27,8 +27,13 @@
 //
 // The re-used z face is the only place the arithmetic is not literally the
 // reference's: -RN(c*(a-b)) equals RN(c*(b-a)) except for the sign of an
-// exact zero, which can only surface as a -0.0 result where the reference
-// has +0.0; the epilogue fixes exactly that case (see fix_negzero).
+// exact zero, which could only surface as a -0.0 result whose lower neighbour
+// holds -0.0 in that unknown (where the reference has +0.0).  Inside the range
+// gate every unknown of every evaluated volume is nonzero, and a sum that
+// starts from a nonzero value can only reach zero by exact cancellation,
+// which rounds to +0.0: a -0.0 result is impossible on the fused path.
+// Patches with zeros leave the gate and are re-evaluated by fvb_redo_kernel,
+// which evaluates every face from both sides exactly as the reference does.
 #include <cuda_runtime.h>
 
 #include <cstdlib>
@@ -110,9 +115,6 @@ __device__ __forceinline__ bool inv_ok(double inv) {
   return inv == 0.0 || (e >= 2u && e < 0x7ffu);
 }
 
-__device__ __forceinline__ bool is_negzero(double v) {
-  return (unsigned long long)__double_as_longlong(v) == 0x8000000000000000ull;
-}
 
 // Plane kinds of the z march (haloed plane index zh = 0 .. 17).
 enum PlaneKind { kZLo = 0, kFirst = 1, kSteady = 2, kZHi = 3 };
@@ -198,7 +200,6 @@ fused3d_kernel(const double* __restrict__ qin, double* __restrict__ qout, const 
     issue(0, 1, 1);
   }
 
-  bool bad = false;
   bool slow = false;           // some quotient of this thread's volumes left the range gate (this patch)
   unsigned long long cm = 0;   // running max wave speed (bit pattern) of this column
   // z-march carries: z-side data of the previous plane, and the previous z face
@@ -241,8 +242,7 @@ fused3d_kernel(const double* __restrict__ qin, double* __restrict__ qout, const 
         if (K == kFirst || K == kSteady) {
           Side<3> sd[3];
           bool ok;
-          const Thermo<3> T = closure_all_ranged<3>(q, cl, sd, ok);
-          bad = bad | (ok & T.bad);
+          closure_all_ranged<3>(q, cl, sd, ok);
           slow = slow | !ok;
           unsigned long long m = (unsigned long long)__double_as_longlong(sd[0].lam);
           unsigned long long v = (unsigned long long)__double_as_longlong(sd[1].lam);
@@ -255,8 +255,7 @@ fused3d_kernel(const double* __restrict__ qin, double* __restrict__ qout, const 
           zcur = sd[2];
         } else {   // z-halo planes: only their z-side data
           bool ok;
-          const Thermo<3> T = closure_one_ranged<3>(q, cl, 2, zcur, ok);
-          bad = bad | (ok & T.bad);
+          closure_one_ranged<3>(q, cl, 2, zcur, ok);
           slow = slow | !ok;
         }
         if (K == kFirst) {
@@ -328,22 +327,6 @@ fused3d_kernel(const double* __restrict__ qin, double* __restrict__ qout, const 
             val[u] = dadd(val[u], dmul(half_inv, dsub(favg_zm[u], sum_p)));
             favg_zm[u] = sum_p;
           }
-          // fix_negzero: the re-used z- term can only differ from the reference's
-          // in the sign of an exact zero, visible solely as a -0.0 result whose
-          // lower neighbour holds -0.0 in the same unknown (then the reference
-          // adds +0.0 and ends at +0.0).  Rare: check the input in HBM.
-          bool nz = false;
-#pragma unroll
-          for (int u = 0; u < S; ++u) nz = nz | is_negzero(val[u]);
-          if (__builtin_expect(nz, 0)) {
-            const int64_t vlow = ((int64_t)(zh - 2) * E + (y + 1)) * E + (x + 1);
-#pragma unroll
-            for (int u = 0; u < S; ++u) {
-              const double qlow =
-                  L == kAoS ? qin[(pidx * VOL + vlow) * S + u] : qin[((int64_t)u * n + pidx) * VOL + vlow];
-              if (is_negzero(val[u]) && is_negzero(qlow)) val[u] = 0.0;
-            }
-          }
           double* ob = outb + (zh & 1) * OUTN;   // output buffer of interior plane zh-2 (parity (zh-2)&1)
 #pragma unroll
           for (int u = 0; u < S; ++u) {
@@ -361,8 +344,7 @@ fused3d_kernel(const double* __restrict__ qin, double* __restrict__ qout, const 
           load_q<L>(st, hy, x + 1, qh);
           Side<3> sh;
           bool ok;
-          const Thermo<3> T = closure_one_ranged<3>(qh, cl, 1, sh, ok);
-          bad = bad | (ok & T.bad);
+          closure_one_ranged<3>(qh, cl, 1, sh, ok);
           slow = slow | !ok;
           put_ys(ys_w, hy, x, sh);
         }
@@ -372,8 +354,7 @@ fused3d_kernel(const double* __restrict__ qin, double* __restrict__ qout, const 
           load_q<L>(st, x + 1, hx, qh);
           Side<3> sh;
           bool ok;
-          const Thermo<3> T = closure_one_ranged<3>(qh, cl, 0, sh, ok);
-          bad = bad | (ok & T.bad);
+          closure_one_ranged<3>(qh, cl, 0, sh, ok);
           slow = slow | !ok;
           put_xs(xs_w, x, hx, sh);
         }
@@ -415,9 +396,7 @@ fused3d_kernel(const double* __restrict__ qin, double* __restrict__ qout, const 
     plane(NPL - 1, Kind<kZHi>{});
   }
 
-  const int any_bad = __syncthreads_or(bad ? 1 : 0);
   if (producer) bulk_wait_all0();
-  if (tid == 0 && any_bad) atomicOr(status, 1u);
 }
 
 static int min_blocks_choice() {

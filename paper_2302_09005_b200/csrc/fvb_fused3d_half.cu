@@ -115,9 +115,6 @@ __device__ __forceinline__ bool inv_ok(double inv) {
   return inv == 0.0 || (e >= 2u && e < 0x7ffu);
 }
 
-__device__ __forceinline__ bool is_negzero(double v) {
-  return (unsigned long long)__double_as_longlong(v) == 0x8000000000000000ull;
-}
 
 enum PlaneKind { kZLo = 0, kFirst = 1, kSteady = 2, kZHi = 3 };
 template <int K>
@@ -210,7 +207,6 @@ fused3d_half_kernel(const double* __restrict__ qin, double* __restrict__ qout, c
     issue(0, 1, 1);
   }
 
-  bool bad = false;
   bool slow = false;
   unsigned long long cm = 0;
   Side<3> zprev;
@@ -250,8 +246,7 @@ fused3d_half_kernel(const double* __restrict__ qin, double* __restrict__ qout, c
         if (K == kFirst || K == kSteady) {
           Side<3> sd[3];
           bool ok;
-          const Thermo<3> T = closure_all_ranged<3>(q, cl, sd, ok);
-          bad = bad | (ok & T.bad);
+          closure_all_ranged<3>(q, cl, sd, ok);
           slow = slow | !ok;
           unsigned long long m = (unsigned long long)__double_as_longlong(sd[0].lam);
           unsigned long long v = (unsigned long long)__double_as_longlong(sd[1].lam);
@@ -272,8 +267,7 @@ fused3d_half_kernel(const double* __restrict__ qin, double* __restrict__ qout, c
           }
         } else {
           bool ok;
-          const Thermo<3> T = closure_one_ranged<3>(q, cl, 2, zcur, ok);
-          bad = bad | (ok & T.bad);
+          closure_one_ranged<3>(q, cl, 2, zcur, ok);
           slow = slow | !ok;
         }
         if (K == kFirst) {
@@ -348,19 +342,6 @@ fused3d_half_kernel(const double* __restrict__ qin, double* __restrict__ qout, c
             val[u] = dadd(val[u], dmul(half_inv, dsub(favg_zm[u], sum_p)));
             favg_zm[u] = sum_p;
           }
-          // fix_negzero (fvb_fused3d.cu)
-          bool nz = false;
-#pragma unroll
-          for (int u = 0; u < S; ++u) nz = nz | is_negzero(val[u]);
-          if (__builtin_expect(nz, 0)) {
-            const int64_t vlow = ((int64_t)(zh - 2) * E + (y0 + ly + 1)) * E + (x + 1);
-#pragma unroll
-            for (int u = 0; u < S; ++u) {
-              const double qlow =
-                  L == kAoS ? qin[(pidx * VOL + vlow) * S + u] : qin[((int64_t)u * n + pidx) * VOL + vlow];
-              if (is_negzero(val[u]) && is_negzero(qlow)) val[u] = 0.0;
-            }
-          }
           double* ob = outb + (zh & 1) * OUTN;
 #pragma unroll
           for (int u = 0; u < S; ++u) {
@@ -380,10 +361,9 @@ fused3d_half_kernel(const double* __restrict__ qin, double* __restrict__ qout, c
           load_q<L>(st, r, x + 1, qh);
           Side<3> sh;
           bool ok;
-          const Thermo<3> T = closure_one_ranged<3>(qh, cl, 1, sh, ok);
+          closure_one_ranged<3>(qh, cl, 1, sh, ok);
           // (the ghost row is also checked by the half that owns it; flagging
           // it twice is harmless)
-          bad = bad | (ok & T.bad);
           slow = slow | !ok;
           put_ys(ys_w, r, x, sh);
         }
@@ -394,8 +374,7 @@ fused3d_half_kernel(const double* __restrict__ qin, double* __restrict__ qout, c
           load_q<L>(st, lr + 1, hx, qh);
           Side<3> sh;
           bool ok;
-          const Thermo<3> T = closure_one_ranged<3>(qh, cl, 0, sh, ok);
-          bad = bad | (ok & T.bad);
+          closure_one_ranged<3>(qh, cl, 0, sh, ok);
           slow = slow | !ok;
           put_xs(xs_w, lr, hx, sh);
         }
@@ -435,13 +414,11 @@ fused3d_half_kernel(const double* __restrict__ qin, double* __restrict__ qout, c
   }
 
   if (OWN_TMEM) tmem_fence_before();
-  const int any_bad = __syncthreads_or(bad ? 1 : 0);
   if (OWN_TMEM) {
     tmem_fence_after();
     if (warp == 0) tmem_dealloc(*tmem_slot, TMEM_COLS);
   }
   if (producer) bulk_wait_all0();
-  if (tid == 0 && any_bad) atomicOr(status, 1u);
 }
 
 template <int L>

@@ -84,9 +84,6 @@ __device__ __forceinline__ bool inv_ok(double inv) {
   const unsigned e = ((unsigned)__double2hiint(inv) >> 20) & 0x7ffu;
   return inv == 0.0 || (e >= 2u && e < 0x7ffu);
 }
-__device__ __forceinline__ bool is_negzero(double v) {
-  return (unsigned long long)__double_as_longlong(v) == 0x8000000000000000ull;
-}
 
 // A y neighbour as the update needs it: state, y wave speed, y fluxes.
 struct YNb {
@@ -187,7 +184,6 @@ fused3d_pair_kernel(const double* __restrict__ qin, double* __restrict__ qout, c
     issue(0, 1, 1);
   }
 
-  bool bad = false;
   bool slow = false;
   unsigned long long cm = 0;
   ZCarry zk[KC];
@@ -226,8 +222,7 @@ fused3d_pair_kernel(const double* __restrict__ qin, double* __restrict__ qout, c
           if (K == kFirst || K == kSteady) {
             Side<3> sd[3];
             bool ok;
-            const Thermo<3> T = closure_all_ranged<3>(q, cl, sd, ok);
-            bad = bad | (ok & T.bad);
+            closure_all_ranged<3>(q, cl, sd, ok);
             slow = slow | !ok;
             unsigned long long m = (unsigned long long)__double_as_longlong(sd[0].lam);
             unsigned long long v = (unsigned long long)__double_as_longlong(sd[1].lam);
@@ -240,8 +235,7 @@ fused3d_pair_kernel(const double* __restrict__ qin, double* __restrict__ qout, c
             zc = sd[2];
           } else {
             bool ok;
-            const Thermo<3> T = closure_one_ranged<3>(q, cl, 2, zc, ok);
-            bad = bad | (ok & T.bad);
+            closure_one_ranged<3>(q, cl, 2, zc, ok);
             slow = slow | !ok;
           }
         };
@@ -310,19 +304,6 @@ fused3d_pair_kernel(const double* __restrict__ qin, double* __restrict__ qout, c
             val[u] = dadd(val[u], dmul(half_inv, dsub(zz.favg[u], sum_p)));
             zz.favg[u] = sum_p;
           }
-          // fix_negzero (fvb_fused3d.cu)
-          bool nz = false;
-#pragma unroll
-          for (int u = 0; u < S; ++u) nz = nz | is_negzero(val[u]);
-          if (__builtin_expect(nz, 0)) {
-            const int64_t vlow = ((int64_t)(zh - 2) * E + (y0 + ly + 1)) * E + (x + 1);
-#pragma unroll
-            for (int u = 0; u < S; ++u) {
-              const double qlow =
-                  L == kAoS ? qin[(pidx * VOL + vlow) * S + u] : qin[((int64_t)u * n + pidx) * VOL + vlow];
-              if (is_negzero(val[u]) && is_negzero(qlow)) val[u] = 0.0;
-            }
-          }
           double* ob_ = outb + (zh & 1) * OUTN;
 #pragma unroll
           for (int u = 0; u < S; ++u) {
@@ -364,8 +345,7 @@ fused3d_pair_kernel(const double* __restrict__ qin, double* __restrict__ qout, c
           load_q<L>(st, r, x + 1, qh);
           Side<3> sh;
           bool ok;
-          const Thermo<3> T = closure_one_ranged<3>(qh, cl, 1, sh, ok);
-          bad = bad | (ok & T.bad);
+          closure_one_ranged<3>(qh, cl, 1, sh, ok);
           slow = slow | !ok;
           put_ys(ys_w, r, x, sh);
         }
@@ -376,8 +356,7 @@ fused3d_pair_kernel(const double* __restrict__ qin, double* __restrict__ qout, c
           load_q<L>(st, lr + 1, hx, qh);
           Side<3> sh;
           bool ok;
-          const Thermo<3> T = closure_one_ranged<3>(qh, cl, 0, sh, ok);
-          bad = bad | (ok & T.bad);
+          closure_one_ranged<3>(qh, cl, 0, sh, ok);
           slow = slow | !ok;
           put_xs(xs_w, lr, hx, sh);
         }
@@ -416,9 +395,7 @@ fused3d_pair_kernel(const double* __restrict__ qin, double* __restrict__ qout, c
     plane(NPL - 1, Kind<kZHi>{});
   }
 
-  const int any_bad = __syncthreads_or(bad ? 1 : 0);
   if (producer) bulk_wait_all0();
-  if (tid == 0 && any_bad) atomicOr(status, 1u);
 }
 
 template <int L>

@@ -77,7 +77,7 @@ __device__ __forceinline__ void put_rec(double* side, int n, int hn, int a, int 
 }
 
 template <int P>
-__global__ void __launch_bounds__(Cfg<P>::THREADS)
+__global__ void __launch_bounds__(Cfg<P>::THREADS, 3)
 small3d_kernel(const double* __restrict__ qin, double* __restrict__ qout, const double* __restrict__ cell_size,
                const double* __restrict__ dtv, double* __restrict__ max_eig, unsigned* __restrict__ status,
                int64_t n_patches, Closure cl) {
@@ -127,7 +127,6 @@ small3d_kernel(const double* __restrict__ qin, double* __restrict__ qout, const 
   if (tid == 0)
     for (int g = 0; g < C::NST && g < G; ++g) issue(g);
 
-  bool bad = false;
   unsigned stg = 0, par = 0;
   // per-patch scalars, loaded one iteration ahead (their latency used to stall the closures)
   auto scalars = [&](int g, double& cs, double& dtp) {
@@ -174,8 +173,7 @@ small3d_kernel(const double* __restrict__ qin, double* __restrict__ qout, const 
       load(cx + 1, cy + 1, cz + 1, q);
       Side<3> sd[3];
       bool ok;
-      const Thermo<3> T = closure_all_ranged<3>(q, cl, sd, ok);
-      bad = bad | (ok & T.bad);
+      closure_all_ranged<3>(q, cl, sd, ok);
       slow = slow | !ok;
       unsigned long long m = (unsigned long long)__double_as_longlong(sd[0].lam);
       unsigned long long v = (unsigned long long)__double_as_longlong(sd[1].lam);
@@ -198,12 +196,10 @@ small3d_kernel(const double* __restrict__ qin, double* __restrict__ qout, const 
         load(hx, hy, hz, qh);
         Side<3> sh;
         bool okh;
-        Thermo<3> Th;
         // nd is warp-uniform (a warp's 32 halo tasks lie on one face pair)
-        if (nd == 0) Th = closure_one_ranged<3>(qh, cl, 0, sh, okh);
-        else if (nd == 1) Th = closure_one_ranged<3>(qh, cl, 1, sh, okh);
-        else Th = closure_one_ranged<3>(qh, cl, 2, sh, okh);
-        bad = bad | (okh & Th.bad);
+        if (nd == 0) closure_one_ranged<3>(qh, cl, 0, sh, okh);
+        else if (nd == 1) closure_one_ranged<3>(qh, cl, 1, sh, okh);
+        else closure_one_ranged<3>(qh, cl, 2, sh, okh);
         slow = slow | !okh;
         put_rec<P>(side, nd, hn, a, b, sh);
       }
@@ -247,7 +243,6 @@ small3d_kernel(const double* __restrict__ qin, double* __restrict__ qout, const 
           val[u] = dadd(val[u], dmul(half_inv, dsub(dadd(fm, fc), dadd(fc, fp))));
         }
       }
-#pragma unroll
       const int lin = (cz * P + cy) * P + cx;   // AoS interior order (x fastest)
 #pragma unroll
       for (int u = 0; u < S; ++u) outb[(g & 1) * C::OUTN + (lp * C::IVOL + lin) * S + u] = val[u];
@@ -286,11 +281,7 @@ small3d_kernel(const double* __restrict__ qin, double* __restrict__ qout, const 
     stg = stg == C::NST - 1 ? 0 : stg + 1;
     par ^= (stg == 0);
   }
-  const int any_bad = __syncthreads_or(bad ? 1 : 0);
-  if (tid == 0) {
-    bulk_wait_all0();
-    if (any_bad) atomicOr(status, 1u);
-  }
+  if (tid == 0) bulk_wait_all0();
 }
 
 template <int P>
