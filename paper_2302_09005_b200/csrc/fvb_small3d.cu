@@ -183,26 +183,36 @@ small3d_kernel(const double* __restrict__ qin, double* __restrict__ qout, const 
       put_rec<P>(side, 0, cx + 1, cy, cz, sd[0]);
       put_rec<P>(side, 1, cy + 1, cx, cz, sd[1]);
       put_rec<P>(side, 2, cz + 1, cx, cy, sd[2]);
-      // ---- A2: face-halo volumes of this patch, one direction each ----
-      for (int h = cell; h < C::NHALO; h += C::IVOL) {
-        const int face = h / (P * P);          // 0: x-, 1: x+, 2: y-, 3: y+, 4: z-, 5: z+
-        const int a = h % P, b = (h / P) % P;  // interior coords across the face normal
-        const int nd = face >> 1;
-        const int hn = (face & 1) ? E - 1 : 0;
+    }
+    // ---- A2: face-halo volumes, one direction each, balanced over the CTA's warps ----
+    // The 2 x 96 tasks form 6 chunks of 32 (one patch slot, one face pair -> a
+    // warp-uniform direction).  Warp w evaluates chunk w whole and half of chunk
+    // 4 + w/2, so every warp does 1.5 passes (a per-patch split would leave one
+    // warp of each patch with two passes and stall the barrier).
+    {
+      static_assert(P == 4 && C::PPC == 2 && C::THREADS == 128, "halo balancing assumes 3D p=4 pairs");
+      auto halo_task = [&](int chunk, int idx) {
+        const int lpt = chunk / 3, nd = chunk % 3;
+        if (lpt >= np) return;
+        const int hn = (idx >> 4) ? E - 1 : 0;
+        const int a = idx & 3, b = (idx >> 2) & 3;   // interior coords across the face normal
         const int hx = nd == 0 ? hn : a + 1;
         const int hy = nd == 1 ? hn : (nd == 0 ? a + 1 : b + 1);
         const int hz = nd == 2 ? hn : b + 1;
+        const double* stt = ring + stg * C::STAGE + lpt * C::VOL * S;
         double qh[S];
-        load(hx, hy, hz, qh);
+#pragma unroll
+        for (int u = 0; u < S; ++u) qh[u] = stt[((hz * E + hy) * E + hx) * S + u];
         Side<3> sh;
         bool okh;
-        // nd is warp-uniform (a warp's 32 halo tasks lie on one face pair)
         if (nd == 0) closure_one_ranged<3>(qh, cl, 0, sh, okh);
         else if (nd == 1) closure_one_ranged<3>(qh, cl, 1, sh, okh);
         else closure_one_ranged<3>(qh, cl, 2, sh, okh);
-        slow = slow | !okh;
-        put_rec<P>(side, nd, hn, a, b, sh);
-      }
+        if (!okh) atomicOr(&slowflag[g & 1], 1u << lpt);   // rare: queue that patch for the exact pass
+        put_rec<P>(sideb + lpt * C::SIDE, nd, hn, a, b, sh);
+      };
+      halo_task(warp, lane);
+      if ((lane >> 4) == (warp & 1)) halo_task(4 + (warp >> 1), lane);
     }
     if (__any_sync(0xffffffffu, slow) && lane == 0) atomicOr(&slowflag[g & 1], 1u << (lp & 31));
     __syncthreads();
