@@ -116,6 +116,10 @@ __device__ __forceinline__ bool inv_ok(double inv) {
 }
 
 
+#ifndef FVB3D_STEADY_UNROLL
+#define FVB3D_STEADY_UNROLL 1
+#endif
+constexpr int STEADY_UNROLL = FVB3D_STEADY_UNROLL;   // unroll of the steady plane loop
 enum PlaneKind { kZLo = 0, kFirst = 1, kSteady = 2, kZHi = 3 };
 template <int K>
 using Kind = std::integral_constant<int, K>;
@@ -217,7 +221,10 @@ fused3d_half_kernel(const double* __restrict__ qin, double* __restrict__ qout, c
 #pragma unroll
   for (int k = 0; k < 4; ++k) zprev.f[k] = 0.0;
 
-  unsigned stg = 0, par = 0;
+  // 18 planes per item and NST = 3: the ring stage of plane zh is zh % 3 and its
+  // mbarrier phase parity (zh / 3) & 1 for every item (each item uses six full
+  // ring cycles), so both follow from zh alone.
+  static_assert(NPL % (2 * NST) == 0, "stage / parity must be item-periodic");
 
   for (int jp = 0; jp < my_items; ++jp) {
     const int64_t it = item_index(jp);
@@ -230,8 +237,10 @@ fused3d_half_kernel(const double* __restrict__ qin, double* __restrict__ qout, c
 
     auto plane = [&](int zh, auto kind) {
       constexpr int K = decltype(kind)::value;
+      const unsigned stg = (unsigned)(zh % NST), par = (unsigned)((zh / NST) & 1);
+      const unsigned stp = stg == 0 ? NST - 1 : stg - 1;   // stage of plane zh-1
       const double* st = ring + stg * STAGE;
-      const double* stc = ring + (stg == 0 ? NST - 1 : stg - 1) * STAGE;
+      const double* stc = ring + stp * STAGE;
       double* ys_w = ysb + (zh & 1) * YS;
       double* xs_w = xsb + (zh & 1) * XS;
       const double* ys_r = ysb + ((zh - 1) & 1) * YS;
@@ -398,17 +407,15 @@ fused3d_half_kernel(const double* __restrict__ qin, double* __restrict__ qout, c
       if (producer) {
         const int zn = zh + 2 < NPL ? zh + 2 : zh + 2 - NPL;
         const int jn = zh + 2 < NPL ? jp : jp + 1;
-        if (jn < my_items) issue(jn, zn, stg == 0 ? NST - 1 : stg - 1);
+        if (jn < my_items) issue(jn, zn, stp);
         if (K == kSteady || K == kZHi) store_out(pidx, y0, zh - 2);
         if (K == kZHi) finish_item(jp, pidx);
       }
-      stg = stg == NST - 1 ? 0 : stg + 1;
-      par ^= (stg == 0);
     };
 
     plane(0, Kind<kZLo>{});
     plane(1, Kind<kFirst>{});
-#pragma unroll 1
+#pragma unroll STEADY_UNROLL
     for (int zh = 2; zh <= P; ++zh) plane(zh, Kind<kSteady>{});
     plane(NPL - 1, Kind<kZHi>{});
   }
