@@ -14,6 +14,7 @@ There is no CPU fallback anywhere: without a CUDA device these raise.
 from __future__ import annotations
 
 import ctypes
+import os
 import threading
 
 import numpy as np
@@ -204,11 +205,15 @@ def _workspace(torch, device, nbytes: int):
     return ws, stream
 
 
-def default_chunk(spec: PatchSpec, n: int) -> int:
+def default_chunk(spec: PatchSpec, n: int, pipeline_chunks: int | None = None) -> int:
+    """Host-pipeline chunk: at most 256 MB of device buffers per set, and about
+    FVB_HOST_CHUNKS (default 32) chunks per call so the unoverlapped first H2D /
+    last D2H (pipeline fill and drain) stay a small fraction of the transfer."""
     per_patch = (spec.haloed_volumes + spec.interior_volumes) * spec.unknowns * 8
     by_bytes = max(1, (256 << 20) // per_patch)
-    by_pipeline = max(1, -(-n // 8))
-    return int(max(1, min(n, by_bytes, max(by_pipeline, min(n, 64)))))
+    k = int(pipeline_chunks or os.environ.get("FVB_HOST_CHUNKS", "32"))
+    by_pipeline = max(1, -(-n // k))
+    return int(max(1, min(n, by_bytes, max(by_pipeline, min(n, 16)))))
 
 
 def update_host(batch: PatchBatch, gamma: float, device=None, kernel="auto", chunk_patches: int | None = None):
