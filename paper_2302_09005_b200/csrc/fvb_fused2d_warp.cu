@@ -239,7 +239,10 @@ fused2d_warp_kernel(const double* __restrict__ qin, double* __restrict__ qout, c
         closure_one_ranged<2>(q, cl, 1, ycur, ok);
         slow = slow | !ok;
       }
-      __syncwarp();   // x-side row hy and the halo batch are visible to the warp
+      // No __syncwarp here: the update below reads only data published in earlier
+      // steps (x-side row hy-1, halo rows <= hy-1), so the closure of row hy and the
+      // update of row hy-1 form one block the scheduler interleaves; the syncwarp at
+      // the end of the step publishes row hy's x-side data and this step's halo batch.
 
       if (hy == 1) {
         // the face (0 | 1): minus face of the first interior row
