@@ -304,7 +304,7 @@ int fvb_halo_project(const fvb_spec* spec, const double* qout, double* qin, cons
 
 size_t fvb_totals_scratch_bytes(const fvb_spec* spec) {
   if (check_spec(spec)) return 0;
-  return (size_t)512 * spec->unknowns * sizeof(double);
+  return (size_t)kTotalsBlocks * spec->unknowns * sizeof(double);
 }
 
 int fvb_totals(const fvb_spec* spec, const double* qout, double* scratch, double* totals, void* stream) {

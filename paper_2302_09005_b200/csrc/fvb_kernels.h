@@ -8,6 +8,8 @@ struct BoxInfo {
   int64_t trig_rho, trig_p, first_nonpos, first_badpl;
 };
 
+constexpr int kTotalsBlocks = 592;   // partial-sum blocks of fvb_totals (scratch = blocks x unknowns doubles)
+
 struct FvbArgs {
   int dim, p, layout;
   int64_t n;

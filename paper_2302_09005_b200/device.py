@@ -167,16 +167,24 @@ class DeviceBatch:
                                                 int(bool(periodic)), _stream_handle(torch, stream)),
                    "fvb_halo_project")
 
+    def totals_scratch(self):
+        """Device scratch for totals_into (fvb_totals_scratch_bytes)."""
+        torch = _torch()
+        L = _lib.load()
+        return torch.empty(L.fvb_totals_scratch_bytes(ctypes.byref(self.fvb_spec())) // 8, dtype=torch.float64,
+                           device=self.device)
+
+    def totals_into(self, out, scratch, stream=None) -> None:
+        """out[u] <- sum of unknown u of QOut over all interior volumes; asynchronous, no host sync."""
+        torch = _torch()
+        _lib.check(_lib.load().fvb_totals(ctypes.byref(self.fvb_spec()), _vp(self.QOut), _vp(scratch), _vp(out),
+                                          _stream_handle(torch, stream)), "fvb_totals")
+
     def totals(self, stream=None) -> np.ndarray:
         """Per-unknown sums of QOut over all interior volumes (conservation diagnostics)."""
         torch = _torch()
-        L = _lib.load()
-        fs = self.fvb_spec()
-        scratch = torch.empty(L.fvb_totals_scratch_bytes(ctypes.byref(fs)) // 8, dtype=torch.float64,
-                              device=self.device)
         out = torch.empty(self.spec.unknowns, dtype=torch.float64, device=self.device)
-        _lib.check(L.fvb_totals(ctypes.byref(fs), _vp(self.QOut), _vp(scratch), _vp(out),
-                                _stream_handle(torch, stream)), "fvb_totals")
+        self.totals_into(out, self.totals_scratch(), stream)
         return out.cpu().numpy()
 
     def to_host(self, batch: PatchBatch) -> None:

@@ -130,29 +130,48 @@ def run_simulation(db: DeviceBatch, grid_shape, steps: int, cfl: float = 0.4, pe
     previous state (a pre-pass for the first step), the fused
     update of every patch, and the halo projection that rebuilds QIn from the
     new QOut (mesh.py:261-310).  Conserved totals are recorded per step.
+
+    Every step is enqueued on the stream without a host synchronisation: dt,
+    the global wave speed, the totals and the non-physical flag of each step
+    land in device histories that are copied back once at the end (a
+    NonPhysicalStateError then names the first failing step).
     """
     import numpy as np
 
-    res = SimulationResult(db.spec.dimensions)
+    torch = _torch()
+    s = db.spec.unknowns
+    dev = db.device
+    f64 = dict(dtype=torch.float64, device=dev)
+    tot_h = torch.empty((steps + 1, s), **f64)
+    gmax_h = torch.empty(steps + 1, **f64)
+    dt_h = torch.empty(max(steps, 1), **f64)
+    flag_h = torch.zeros(max(steps, 1), dtype=torch.int32, device=dev)
+    scratch = db.totals_scratch()
+
     db.halo_project(grid_shape, periodic)
+    db.status.zero_()
     stepper = CflStepper(db, cfl=cfl, dx=dx, kernel=kernel)
     stepper.prepass()
-    res.totals.append(db.totals())
-    res.t.append(0.0)
-    res.max_eigenvalue.append(float(stepper.gmax.item()))
-    t = 0.0
-    for _ in range(steps):
-        dt = float(stepper.dt_scalar.item())
-        db.update(kernel=kernel)
-        if db.nonphysical():
-            from .errors import NonPhysicalStateError
-            raise NonPhysicalStateError("non-physical state during run_simulation", step=len(res.dt))
-        stepper.reduce_dt()                       # next step's dt from this step's wave speeds
+    db.totals_into(tot_h[0], scratch)
+    gmax_h[0].copy_(stepper.gmax[0])
+    for k in range(steps):
+        dt_h[k].copy_(stepper.dt_scalar[0])   # the dt this step advances by
+        db.status[1:2].zero_()                # redo count of this launch; status[0] accumulates
+        db.update(kernel=kernel, zero_status=False)
+        flag_h[k].copy_(db.status[0])
+        stepper.reduce_dt()                   # next step's dt from this step's wave speeds
         db.halo_project(grid_shape, periodic)
-        t += dt
-        res.dt.append(dt)
-        res.t.append(t)
-        res.max_eigenvalue.append(float(stepper.gmax.item()))
-        res.totals.append(db.totals())
-    res.totals = list(np.asarray(res.totals))
+        gmax_h[k + 1].copy_(stepper.gmax[0])
+        db.totals_into(tot_h[k + 1], scratch)
+
+    flags = flag_h.cpu().numpy()[:steps]
+    bad = np.flatnonzero(flags)
+    if bad.size:
+        from .errors import NonPhysicalStateError
+        raise NonPhysicalStateError("non-physical state during run_simulation", step=int(bad[0]))
+    res = SimulationResult(db.spec.dimensions)
+    res.dt = [float(v) for v in dt_h.cpu().numpy()[:steps]]
+    res.t = [0.0] + [float(v) for v in np.cumsum(res.dt)]
+    res.max_eigenvalue = [float(v) for v in gmax_h.cpu().numpy()]
+    res.totals = list(tot_h.cpu().numpy())
     return res
