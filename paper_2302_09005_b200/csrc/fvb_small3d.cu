@@ -1,14 +1,14 @@
 // fvb_small3d.cu -- fused 3D Rusanov update for small patches (p = 4: BASELINE
 // config 4, 1M patches).
 //
-// A persistent CTA of 128 threads processes PPC = 2 patches per iteration
-// (one thread per interior cell).  The haloed patches of an iteration are
-// contiguous in HBM (AoS) and arrive with ONE TMA bulk copy into a 2-stage
-// ring.  Per iteration:
+// A persistent CTA of 64 threads processes PPC = 1 patch per iteration (one
+// thread per interior cell; 6 CTAs per SM).  The haloed patch(es) of an
+// iteration are contiguous in HBM (AoS) and arrive with ONE TMA bulk copy into
+// a 2-stage ring.  Per iteration:
 //   A  every thread evaluates the closure of its interior volume (all three
-//      directions) and, in a second pass, the one-direction closures of the
-//      96 face-halo volumes of its patch are spread over the 64 threads;
-//      side data (lam, f[1..4]) goes to per-direction shared arrays. -- barrier
+//      directions); the one-direction closures of the 96 face-halo volumes
+//      are balanced over the warps (1.5 passes each); side data (lam,
+//      f[1..4]) goes to per-direction shared arrays.            -- barrier
 //   B  every cell accumulates its six face terms from the side arrays in the
 //      reference order (vectorized.py:161-200) and writes the interior to a
 //      staging buffer stored with one TMA bulk store per iteration. -- barrier
@@ -32,7 +32,12 @@ struct Cfg {
   static constexpr int E = P + 2;
   static constexpr int VOL = E * E * E;             // haloed volumes per patch
   static constexpr int IVOL = P * P * P;            // interior cells per patch
-  static constexpr int PPC = 128 / IVOL > 0 ? 128 / IVOL : 1;   // patches per CTA iteration
+#ifndef FVB_SMALL3D_PPC
+#define FVB_SMALL3D_PPC 1
+#endif
+  // patches per CTA iteration: 1 (64 threads, ~34 KB, 6 CTAs/SM) measured 11 % faster than
+  // 2 (128 threads, 3 CTAs/SM) -- barriers over two warps, twice the independent CTAs
+  static constexpr int PPC = FVB_SMALL3D_PPC;
   static constexpr int THREADS = PPC * IVOL;
   static constexpr int NHALO = 6 * P * P;           // face-halo volumes per patch
   static constexpr int LINE = E * P * P;            // records of one direction: (E along n) x P x P
@@ -77,7 +82,7 @@ __device__ __forceinline__ void put_rec(double* side, int n, int hn, int a, int 
 }
 
 template <int P>
-__global__ void __launch_bounds__(Cfg<P>::THREADS, 3)
+__global__ void __launch_bounds__(Cfg<P>::THREADS, 6 / Cfg<P>::PPC)
 small3d_kernel(const double* __restrict__ qin, double* __restrict__ qout, const double* __restrict__ cell_size,
                const double* __restrict__ dtv, double* __restrict__ max_eig, unsigned* __restrict__ status,
                int64_t n_patches, Closure cl) {
@@ -185,12 +190,12 @@ small3d_kernel(const double* __restrict__ qin, double* __restrict__ qout, const 
       put_rec<P>(side, 2, cz + 1, cx, cy, sd[2]);
     }
     // ---- A2: face-halo volumes, one direction each, balanced over the CTA's warps ----
-    // The 2 x 96 tasks form 6 chunks of 32 (one patch slot, one face pair -> a
+    // The PPC x 96 tasks form 3*PPC chunks of 32 (one patch slot, one face pair -> a
     // warp-uniform direction).  Warp w evaluates chunk w whole and half of chunk
-    // 4 + w/2, so every warp does 1.5 passes (a per-patch split would leave one
+    // 2*PPC + w/2, so every warp does 1.5 passes (a per-patch split would leave one
     // warp of each patch with two passes and stall the barrier).
     {
-      static_assert(P == 4 && C::PPC == 2 && C::THREADS == 128, "halo balancing assumes 3D p=4 pairs");
+      static_assert(P == 4 && C::THREADS == 64 * C::PPC, "halo balancing assumes 3D p=4");
       auto halo_task = [&](int chunk, int idx) {
         const int lpt = chunk / 3, nd = chunk % 3;
         if (lpt >= np) return;
@@ -211,8 +216,8 @@ small3d_kernel(const double* __restrict__ qin, double* __restrict__ qout, const 
         if (!okh) atomicOr(&slowflag[g & 1], 1u << lpt);   // rare: queue that patch for the exact pass
         put_rec<P>(sideb + lpt * C::SIDE, nd, hn, a, b, sh);
       };
-      halo_task(warp, lane);
-      if ((lane >> 4) == (warp & 1)) halo_task(4 + (warp >> 1), lane);
+      halo_task(warp, lane);   // chunks 0 .. 2*PPC-1 whole, chunks 2*PPC .. 3*PPC-1 in halves
+      if ((lane >> 4) == (warp & 1)) halo_task(2 * C::PPC + (warp >> 1), lane);
     }
     if (__any_sync(0xffffffffu, slow) && lane == 0) atomicOr(&slowflag[g & 1], 1u << (lp & 31));
     __syncthreads();
