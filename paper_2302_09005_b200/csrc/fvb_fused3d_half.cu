@@ -39,7 +39,12 @@ namespace f3h {
 using namespace f16;
 
 constexpr int P = 16, E = 18, S = 5;
-constexpr int R = 8;                      // interior rows per half
+#ifndef FVB3D_HALF_ROWS
+#define FVB3D_HALF_ROWS 8
+#endif
+constexpr int R = FVB3D_HALF_ROWS;        // interior rows per CTA work item (8: half patches, 4: quarters)
+constexpr int IPP = P / R;                // work items per patch
+constexpr int NIW = R / 2;                // interior warps (a warp covers two rows)
 constexpr int SR = R + 2;                 // stage rows (halo/ghost above and below)
 constexpr int PLANE = E * E;              // haloed volumes per plane (global layout)
 constexpr int SVOL = SR * E;              // volumes per stage
@@ -51,7 +56,7 @@ constexpr int64_t IVOL = (int64_t)P * P * P;
 constexpr int YS = S * SR * P;            // ys: [c][stage row 0..9][x 0..15]
 constexpr int XS = S * R * E;             // xs: [c][local row 0..7][hx 0..17]
 constexpr int OUTN = R * P * S;           // one output half-plane
-constexpr int NTHREADS = 160;
+constexpr int NTHREADS = 32 * (NIW + 1);   // interior warps + the halo / producer warp
 constexpr int OFF_RING = 0;
 constexpr int OFF_YS = OFF_RING + NST * STAGE;
 constexpr int OFF_XS = OFF_YS + 2 * YS;
@@ -125,7 +130,7 @@ template <int K>
 using Kind = std::integral_constant<int, K>;
 
 template <int L>
-__global__ void __launch_bounds__(NTHREADS, 4)
+__global__ void __launch_bounds__(NTHREADS, R == 8 ? 4 : 7)
 fused3d_half_kernel(const double* __restrict__ qin, double* __restrict__ qout, const double* __restrict__ cell_size,
                     const double* __restrict__ dtv, double* __restrict__ max_eig, unsigned* __restrict__ status,
                     int64_t n, Closure cl) {
@@ -140,20 +145,20 @@ fused3d_half_kernel(const double* __restrict__ qin, double* __restrict__ qout, c
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sm + OFF_TMEM);
 
   const int tid = threadIdx.x;
-  const bool interior = tid < 128;
+  const bool interior = tid < 32 * NIW;
   const int warp = tid >> 5, lane = tid & 31;
   const int x = lane & 15;
-  const int ly = ((warp & 3) << 1) | (lane >> 4);   // local interior row 0..7
-  const bool producer = tid == 128;
+  const int ly = (warp << 1) | (lane >> 4);   // local interior row 0..R-1 (interior warps)
+  const bool producer = tid == 32 * NIW;
 
-  const int64_t items = 2 * n;   // (patch, half) work items
+  const int64_t items = IPP * n;   // (patch, row block) work items
   const int my_items = (items > (int64_t)blockIdx.x) ? (int)((items - 1 - (int64_t)blockIdx.x) / gridDim.x + 1) : 0;
   auto item_index = [&](int j) -> int64_t { return (int64_t)blockIdx.x + (int64_t)j * gridDim.x; };
 
   auto issue = [&](int j, int zh, unsigned s) {
     const int64_t it = item_index(j);
-    const int64_t pidx = it >> 1;
-    const int y0 = (int)(it & 1) * R;
+    const int64_t pidx = it / IPP;
+    const int y0 = (int)(it % IPP) * R;
     double* st = ring + s * STAGE;
     uint64_t* bar = bars + s;
     fence_proxy_async();
@@ -180,10 +185,10 @@ fused3d_half_kernel(const double* __restrict__ qin, double* __restrict__ qout, c
     bulk_commit();
   };
   auto finish_item = [&](int j, int64_t pidx) {
-    unsigned long long m = wmax[(j & 1) * 4];
+    unsigned long long m = wmax[(j & 1) * NIW];
 #pragma unroll
-    for (int w = 1; w < 4; ++w) {
-      const unsigned long long v = wmax[(j & 1) * 4 + w];
+    for (int w = 1; w < NIW; ++w) {
+      const unsigned long long v = wmax[(j & 1) * NIW + w];
       m = v > m ? v : m;
     }
     atomicMax(reinterpret_cast<unsigned long long*>(max_eig) + pidx, m);
@@ -228,8 +233,8 @@ fused3d_half_kernel(const double* __restrict__ qin, double* __restrict__ qout, c
 
   for (int jp = 0; jp < my_items; ++jp) {
     const int64_t it = item_index(jp);
-    const int64_t pidx = it >> 1;
-    const int y0 = (int)(it & 1) * R;
+    const int64_t pidx = it / IPP;
+    const int y0 = (int)(it % IPP) * R;
     const double dx = __ddiv_rn(cell_size[pidx * 3], (double)P);   // vectorized.py:169
     const double inv = __ddiv_rn(dtv[pidx], dx);                    // vectorized.py:170
     const double half_inv = dmul(0.5, inv);
@@ -376,9 +381,9 @@ fused3d_half_kernel(const double* __restrict__ qin, double* __restrict__ qout, c
           slow = slow | !ok;
           put_ys(ys_w, r, x, sh);
         }
-        if (lane < 16) {   // x-face halo columns (hx = 0, 17) of the 8 interior rows
-          const int lr = lane & 7;
-          const int hx = lane < 8 ? 0 : E - 1;
+        if (lane < 2 * R) {   // x-face halo columns (hx = 0, 17) of the R interior rows
+          const int lr = lane % R;
+          const int hx = lane < R ? 0 : E - 1;
           double qh[S];
           load_q<L>(st, lr + 1, hx, qh);
           Side<3> sh;
@@ -398,7 +403,7 @@ fused3d_half_kernel(const double* __restrict__ qin, double* __restrict__ qout, c
             const unsigned long long v = __shfl_xor_sync(0xffffffffu, m, o);
             m = v > m ? v : m;
           }
-          if (lane == 0) wmax[(jp & 1) * 4 + warp] = m;
+          if (lane == 0) wmax[(jp & 1) * NIW + warp] = m;
           cm = 0;
         }
       }
@@ -442,7 +447,7 @@ cudaError_t launch_impl(const FvbArgs& a, cudaStream_t st) {
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kfn, NTHREADS, BYTES);
   if (per_sm < 1) per_sm = 1;
   int64_t grid = (int64_t)sms * per_sm;
-  if (grid > 2 * a.n) grid = 2 * a.n;
+  if (grid > IPP * a.n) grid = IPP * a.n;
   const Closure cl{a.gamma, a.gamma - 1.0};
   kfn<<<(unsigned)grid, NTHREADS, BYTES, st>>>(a.qin, a.qout, a.cell_size, a.dt, a.max_eig, a.status, a.n, cl);
   return cudaGetLastError();
