@@ -32,6 +32,9 @@ struct Cfg {
   static constexpr int E = P + 2;
   static constexpr int VOL = E * E * E;             // haloed volumes per patch
   static constexpr int IVOL = P * P * P;            // interior cells per patch
+#ifndef FVB_SMALL3D_NOB
+#define FVB_SMALL3D_NOB 2
+#endif
 #ifndef FVB_SMALL3D_PPC
 #define FVB_SMALL3D_PPC 1
 #endif
@@ -48,7 +51,10 @@ struct Cfg {
   static constexpr int OFF_RING = 0;
   static constexpr int OFF_SIDE = OFF_RING + NST * STAGE;
   static constexpr int OFF_OUT = OFF_SIDE + PPC * SIDE;
-  static constexpr int OFF_WMAX = OFF_OUT + 2 * OUTN;   // output staging double-buffered
+  // output staging: NOB buffers (1: the store of iteration g-1 must have read it
+  // before phase B of iteration g writes; checked before the mid-iteration barrier)
+  static constexpr int NOB = FVB_SMALL3D_NOB;
+  static constexpr int OFF_WMAX = OFF_OUT + NOB * OUTN;
   static constexpr int OFF_FLAG = OFF_WMAX + 2 * (THREADS / 32);   // wmax double-buffered
   static constexpr int OFF_BAR = OFF_FLAG + 1;   // two 32-bit flag words
   static constexpr int TOTAL = OFF_BAR + NST;
@@ -220,6 +226,7 @@ small3d_kernel(const double* __restrict__ qin, double* __restrict__ qout, const 
       if ((lane >> 4) == (warp & 1)) halo_task(2 * C::PPC + (warp >> 1), lane);
     }
     if (__any_sync(0xffffffffu, slow) && lane == 0) atomicOr(&slowflag[g & 1], 1u << (lp & 31));
+    if (C::NOB == 1 && tid == 0) bulk_wait_read0();   // the single staging buffer, stored last iteration, is free
     __syncthreads();
 
     // ---- B: face terms and update of this thread's cell ----
@@ -260,7 +267,7 @@ small3d_kernel(const double* __restrict__ qin, double* __restrict__ qout, const 
       }
       const int lin = (cz * P + cy) * P + cx;   // AoS interior order (x fastest)
 #pragma unroll
-      for (int u = 0; u < S; ++u) outb[(g & 1) * C::OUTN + (lp * C::IVOL + lin) * S + u] = val[u];
+      for (int u = 0; u < S; ++u) outb[(g % C::NOB) * C::OUTN + (lp * C::IVOL + lin) * S + u] = val[u];
       fence_proxy_async();
     }
     // per-patch max wave speed: 64-bit max as (high word, low word) warp reductions
@@ -270,11 +277,11 @@ small3d_kernel(const double* __restrict__ qin, double* __restrict__ qout, const 
       const unsigned mlo = __reduce_max_sync(0xffffffffu, hi == mhi ? lo : 0u);
       if (lane == 0) wmax[(g & 1) * (C::THREADS / 32) + warp] = ((unsigned long long)mhi << 32) | mlo;
     }
-    if (tid == 0) bulk_wait_read0();   // staging buffer (g & 1) was stored two iterations ago
+    if (C::NOB == 2 && tid == 0) bulk_wait_read0();   // staging buffer (g & 1) was stored two iterations ago
     __syncthreads();
     if (tid == 0) {
       // output of this group, per-patch maxima, redo list; then refill the freed stage
-      tma_store_1d(qout + grp * C::PPC * (int64_t)C::IVOL * S, outb + (g & 1) * C::OUTN,
+      tma_store_1d(qout + grp * C::PPC * (int64_t)C::IVOL * S, outb + (g % C::NOB) * C::OUTN,
                    (uint32_t)(np * C::IVOL * S * 8));
       bulk_commit();
       const unsigned flags = slowflag[g & 1];
