@@ -130,7 +130,10 @@ template <int K>
 using Kind = std::integral_constant<int, K>;
 
 template <int L>
-__global__ void __launch_bounds__(NTHREADS, R == 8 ? 4 : 7)
+#ifndef FVB3D_HALF_MINB
+#define FVB3D_HALF_MINB (R == 8 ? 4 : 7)
+#endif
+__global__ void __launch_bounds__(NTHREADS, FVB3D_HALF_MINB)
 fused3d_half_kernel(const double* __restrict__ qin, double* __restrict__ qout, const double* __restrict__ cell_size,
                     const double* __restrict__ dtv, double* __restrict__ max_eig, unsigned* __restrict__ status,
                     int64_t n, Closure cl) {
