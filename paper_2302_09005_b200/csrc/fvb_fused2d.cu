@@ -320,7 +320,10 @@ cudaError_t launch(const FvbArgs& a, cudaStream_t st) {
 }  // namespace f2
 }  // namespace fvb
 
+// Shapes with a fused kernel: 3D p=16 (AoS/SoA), 3D p=4 (AoS), 2D p=16 (AoS/SoA)
+// and 2D p=2..32 (AoS, the warp kernel); everything else runs the generic kernel.
 bool fvb_fused16_supported(int dim, int p, int layout) {
+  if (dim == 2 && layout == fvb::kAoS && fvb_fused2d_warp_supported(p)) return true;
   return (p == 16 && (dim == 2 || dim == 3) && (layout == fvb::kAoS || layout == fvb::kSoA)) ||
          fvb_small3d_supported(dim, p, layout);
 }
@@ -351,14 +354,16 @@ bool fvb_fused2d_use_warp() {
 cudaError_t fvb_launch_fused16(const FvbArgs& a, cudaStream_t st) {
   using namespace fvb;
   if (a.n <= 0) return cudaSuccess;
-  if (a.p != 16) return fvb_launch_small3d(a, st);   // includes its redo pass
+  if (a.dim == 3 && a.p != 16) return fvb_launch_small3d(a, st);   // includes its redo pass
   cudaError_t e;
   if (a.dim == 3) {
     const int c = fvb_fused3d_choice();
     e = c == 0 ? fvb_launch_fused3d16(a, st) : c == 2 ? fvb_launch_fused3d16_pair(a, st) : fvb_launch_fused3d16_half(a, st);
+  } else if (a.layout == kAoS && (a.p != 16 || fvb_fused2d_use_warp())) {
+    e = fvb_launch_fused2d16_warp(a, st);
+  } else {
+    e = a.layout == kAoS ? f2::launch<kAoS>(a, st) : f2::launch<kSoA>(a, st);
   }
-  else if (a.layout == kAoS && fvb_fused2d_use_warp()) e = fvb_launch_fused2d16_warp(a, st);
-  else e = a.layout == kAoS ? f2::launch<kAoS>(a, st) : f2::launch<kSoA>(a, st);
   if (e != cudaSuccess) return e;
   return fvb_launch_redo(a, st);   // exact re-evaluation of queued patches (usually none)
 }

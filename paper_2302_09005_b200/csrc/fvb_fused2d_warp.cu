@@ -38,33 +38,42 @@ namespace f2w {
 
 using namespace f16;
 
-constexpr int P = 16, E = 18, S = 4;
-constexpr int64_t VOL = (int64_t)E * E;
-constexpr int64_t IVOL = (int64_t)P * P;
-constexpr int ROWD = E * S;               // doubles per haloed patch row (576 B)
-constexpr int OFFB = 82;                  // patch-B row offset in a stage: 656 B = 16 mod 128
-constexpr int STGD = 154;                 // stage: two rows + padding (1,232 B)
-constexpr int NS = 7;                     // ring stages per warp
-constexpr int HB = 4;                     // halo-column rows per batch (16 lanes)
-constexpr int XSD = 4 * 32;               // x-side row: [c][lane]
-constexpr int HXR = 8;                    // halo x-side ring rows
-constexpr int HXC = HXR * 4;              // halo x-side doubles per component: [row slot][side][patch slot]
-constexpr int HXS = 4 * HXC;              // [c][row slot][side][patch slot]
-constexpr int OUTR = P * S;               // one output row of one patch (512 B)
-constexpr int OFFO = 130;                 // patch-B output offset: 1,040 B = 16 mod 128
-constexpr int OUTD = OFFO + 2 * OUTR;     // output staging: two rows of each patch, stored together
+// Per-P configuration.  P <= 16: two patches per warp (lane l -> slot l & 1,
+// column l >> 1); 16 < P <= 32: one patch per warp (lane = column).  Lanes
+// whose column is >= P idle through the march (their results are discarded).
+template <int P_>
+struct W2 {
+  static constexpr int P = P_, E = P + 2, S = 4;
+  static constexpr int PPW = P <= 16 ? 2 : 1;                    // patches per warp
+  static constexpr int64_t VOL = (int64_t)E * E;
+  static constexpr int64_t IVOL = (int64_t)P * P;
+  static constexpr int ROWD = E * S;                             // doubles per haloed patch row
+  static constexpr int OFFB = (ROWD + 15) / 16 * 16 + 2;         // patch-B row offset: 16 B mod 128 B
+  static constexpr int STGD = PPW == 2 ? (OFFB + ROWD + 1) / 2 * 2 : (ROWD + 1) / 2 * 2;   // stage (16 B multiple)
+  static constexpr int NS = 7;                                   // ring stages per warp
+  static constexpr int HB = 4;                                   // halo-column rows per batch
+  static constexpr int XSD = 4 * 32;                             // x-side row: [c][lane]
+  static constexpr int HXR = 8;                                  // halo x-side ring rows
+  static constexpr int HXC = HXR * 4;                            // per component: [row slot][side][patch slot]
+  static constexpr int HXS = 4 * HXC;
+  static constexpr int OUTR = P * S;                             // one output row of one patch
+  static constexpr int OFFO = (2 * OUTR + 15) / 16 * 16 + 2;     // patch-B output offset: 16 B mod 128 B
+  static constexpr int OUTD = PPW == 2 ? OFFO + 2 * OUTR : 2 * OUTR;   // two rows of each patch, stored together
+  static constexpr int W_RING = 0;
+  static constexpr int W_XS = W_RING + NS * STGD;
+  static constexpr int W_HX = W_XS + 2 * XSD;
+  static constexpr int W_OUT = W_HX + HXS;
+  static constexpr int W_BAR = W_OUT + OUTD;
+  static constexpr int WARPD = (W_BAR + NS + 1) & ~1;            // doubles per warp (16 B multiple)
+};
+constexpr int S = 4;
 constexpr int WPC = 4;                    // warps per CTA
 #ifndef FVB2D_HY_UNROLL
 #define FVB2D_HY_UNROLL 2
 #endif
 constexpr int HY_UNROLL = FVB2D_HY_UNROLL;
-constexpr int W_RING = 0;
-constexpr int W_XS = W_RING + NS * STGD;
-constexpr int W_HX = W_XS + 2 * XSD;
-constexpr int W_OUT = W_HX + HXS;
-constexpr int W_BAR = W_OUT + OUTD;
-constexpr int WARPD = (W_BAR + NS + 1) & ~1;   // doubles per warp (16 B multiple)
-constexpr size_t BYTES = (size_t)WPC * WARPD * 8;
+template <int P>
+constexpr size_t bytes_of() { return (size_t)WPC * W2<P>::WARPD * 8; }
 
 __device__ __forceinline__ void lds_q(const double* p, double (&q)[S]) {
   const double2 a = *reinterpret_cast<const double2*>(p);
@@ -80,10 +89,17 @@ __device__ __forceinline__ bool inv_ok(double inv) {
   return inv == 0.0 || (e >= 2u && e < 0x7ffu);
 }
 
+template <int P>
 __global__ void __launch_bounds__(WPC * 32, 4)
 fused2d_warp_kernel(const double* __restrict__ qin, double* __restrict__ qout, const double* __restrict__ cell_size,
                     const double* __restrict__ dtv, double* __restrict__ max_eig, unsigned* __restrict__ status,
                     int64_t n, Closure cl) {
+  using C = W2<P>;
+  constexpr int E = C::E, PPW = C::PPW, ROWD = C::ROWD, OFFB = C::OFFB, STGD = C::STGD, NS = C::NS, HB = C::HB;
+  constexpr int XSD = C::XSD, HXR = C::HXR, HXC = C::HXC, OUTR = C::OUTR, OFFO = C::OFFO;
+  constexpr int64_t VOL = C::VOL, IVOL = C::IVOL;
+  constexpr int WARPD = C::WARPD, W_RING = C::W_RING, W_XS = C::W_XS, W_HX = C::W_HX, W_OUT = C::W_OUT,
+                W_BAR = C::W_BAR;
   extern __shared__ __align__(128) double sm[];
   const int warp = threadIdx.x >> 5, l = threadIdx.x & 31;
   double* wb = sm + warp * WARPD;
@@ -93,9 +109,12 @@ fused2d_warp_kernel(const double* __restrict__ qin, double* __restrict__ qout, c
   double* outb = wb + W_OUT;
   uint64_t* bars = reinterpret_cast<uint64_t*>(wb + W_BAR);
 
-  const int ps = l & 1;          // patch slot
-  const int x = l >> 1;          // interior column 0..15
-  const int64_t items = (n + 1) >> 1;
+  const int ps = PPW == 2 ? (l & 1) : 0;          // patch slot
+  const int xl = PPW == 2 ? (l >> 1) : l;         // interior column of this lane
+  const bool act = xl < P;                        // lanes past the last column idle
+  const int x = act ? xl : P - 1;                 // (addressing only)
+  constexpr int LST = PPW;                        // lane step between x neighbours
+  const int64_t items = (n + PPW - 1) / PPW;
   const int64_t gw = (int64_t)blockIdx.x * WPC + warp;
   const int64_t tw = (int64_t)gridDim.x * WPC;
   const int my_items = items > gw ? (int)((items - 1 - gw) / tw + 1) : 0;
@@ -104,9 +123,9 @@ fused2d_warp_kernel(const double* __restrict__ qin, double* __restrict__ qout, c
   // Lane 0's issue cursor: the next haloed row to load (item ij, row ihy) and
   // its ring stage / patch pair, advanced incrementally (no divisions).
   int ij = 0, ihy = 0, is = 0, iissued = 0;
-  int64_t ipa = 2 * gw;
+  int64_t ipa = PPW * gw;
   auto issue_next = [&]() {
-    const bool vb = ipa + 1 < n;
+    const bool vb = PPW == 2 && ipa + 1 < n;
     double* st = ring + is * STGD;
     uint64_t* bar = bars + is;
     fence_proxy_async();
@@ -118,7 +137,7 @@ fused2d_warp_kernel(const double* __restrict__ qin, double* __restrict__ qout, c
     if (++ihy == E) {
       ihy = 0;
       ++ij;
-      ipa += 2 * tw;
+      ipa += PPW * tw;
     }
   };
 
@@ -137,6 +156,8 @@ fused2d_warp_kernel(const double* __restrict__ qin, double* __restrict__ qout, c
   const int right = ps * OFFB + (x + 2) * S;        // x+1 neighbour
   const bool lh = x == 0, rh = x == P - 1;          // neighbour is a face-halo column
   const int lcs = lh ? HXC : 32, rcs = rh ? HXC : 32;   // component strides of the neighbours' x-side data
+  (void)lcs;
+  (void)rcs;
 
   int s = 0;          // ring stage of the current row
   unsigned par = 0;   // its mbarrier phase parity
@@ -147,7 +168,7 @@ fused2d_warp_kernel(const double* __restrict__ qin, double* __restrict__ qout, c
     cs = 1.0;
     dtp = 0.0;
     if (j < my_items) {
-      const int64_t pa = 2 * (gw + (int64_t)j * tw);
+      const int64_t pa = PPW * (gw + (int64_t)j * tw);
       const int64_t pi = pa + ps < n ? pa + ps : pa;
       cs = __ldg(cell_size + pi * 2);
       dtp = __ldg(dtv + pi);
@@ -156,9 +177,9 @@ fused2d_warp_kernel(const double* __restrict__ qin, double* __restrict__ qout, c
   double cs_next, dt_next;
   scalars(0, cs_next, dt_next);
   for (int j = 0; j < my_items; ++j) {
-    const int64_t pa = 2 * (gw + (int64_t)j * tw);
+    const int64_t pa = PPW * (gw + (int64_t)j * tw);
     const int64_t pidx = pa + ps;
-    const bool valid = pidx < n;
+    const bool valid = pidx < n && act;
     const int64_t pl = valid ? pidx : pa;
     const double cs_cur = cs_next, dt_cur = dt_next;
     scalars(j + 1, cs_next, dt_next);
@@ -166,6 +187,7 @@ fused2d_warp_kernel(const double* __restrict__ qin, double* __restrict__ qout, c
     const double inv = __ddiv_rn(dt_cur, dx);          // vectorized.py:170
     const double half_inv = dmul(0.5, inv);
     bool slow = !inv_ok(inv);
+    bool hslow = false;   // halo-batch gate failures, for patch slot l % PPW
     unsigned long long cm = 0;
 
     // y-march carries (row hy-1): own state and x-side data, y-side data,
@@ -185,15 +207,15 @@ fused2d_warp_kernel(const double* __restrict__ qin, double* __restrict__ qout, c
       const double* stp = ring + (s == 0 ? NS - 1 : s - 1) * STGD;   // row hy-1
       mbar_wait(&bars[s], par);
 
-      // ---- halo columns hx = 0, 17 of rows hy .. hy+3 (x-side data only) ----
-      if ((hy & 3) == 1 && hy < E - 1) {
+      // ---- halo columns hx = 0, P+1 of rows hy .. min(hy+3, P) (x-side data only) ----
+      if ((hy & 3) == 1 && hy <= P) {
 #pragma unroll
         for (int d = 1; d < HB; ++d) {
           const int sd = s + d;
-          mbar_wait(&bars[sd >= NS ? sd - NS : sd], par ^ (sd >= NS ? 1u : 0u));
+          if (hy + d <= P) mbar_wait(&bars[sd >= NS ? sd - NS : sd], par ^ (sd >= NS ? 1u : 0u));
         }
-        if (l < 16) {
-          const int hps = l & 1, side = (l >> 1) & 1, dr = l >> 2;
+        const int hps = l % PPW, side = (l / PPW) & 1, dr = l / (2 * PPW);
+        if (l < 2 * PPW * HB && hy + dr <= P) {
           const int sd = s + dr;
           const double* hst = ring + (sd >= NS ? sd - NS : sd) * STGD + hps * OFFB;
           double qh[S];
@@ -207,8 +229,7 @@ fused2d_warp_kernel(const double* __restrict__ qin, double* __restrict__ qout, c
           for (int k = 0; k < 3; ++k) hxs[(k + 1) * HXC + idx] = sh.f[k];
           // a halo volume outside the range gate invalidates its patch: a lane
           // with the same slot carries it into the per-patch vote
-          const unsigned m = __ballot_sync(0xffffu, !ok);
-          slow = slow | ((m & (ps ? 0xaaaau : 0x5555u)) != 0u);
+          hslow = hslow | !ok;   // a halo volume outside the gate invalidates patch slot hps
         }
       }
 
@@ -257,8 +278,8 @@ fused2d_warp_kernel(const double* __restrict__ qin, double* __restrict__ qout, c
         // ---- update of this lane's cell of row hy-1 (interior row hy-2) ----
         const double* xr = xsb + ((hy - 1) & 1) * XSD;
         const double* hr = hxs + ((hy - 2) & (HXR - 1)) * 4 + ps;   // halo x-side of row hy-1, side 0
-        const double* ml = lh ? hr : xr + (l - 2);
-        const double* mr = rh ? hr + 2 : xr + (l + 2);
+        const double* ml = lh ? hr : xr + (l - LST);
+        const double* mr = rh ? hr + 2 : xr + (l + LST);
         double val[S], qn[S];
 #pragma unroll
         for (int u = 0; u < S; ++u) val[u] = oq[u];                        // _pass_copy
@@ -300,14 +321,15 @@ fused2d_warp_kernel(const double* __restrict__ qin, double* __restrict__ qout, c
           if (l == 0) bulk_wait_read<0>();
           __syncwarp();
         }
-        sts_q(outb + ps * OFFO + (z & 1) * OUTR + x * S, val);
-        if (z & 1) {
+        if (act) sts_q(outb + ps * OFFO + (z & 1) * OUTR + x * S, val);
+        if ((z & 1) || z == P - 1) {   // a full pair, or the last row of an odd P
+          const int nr = (z & 1) ? 2 : 1, z0 = z - (nr - 1);
           fence_proxy_async();
           __syncwarp();
           if (l == 0) {
-            tma_store_1d(qout + (pa * IVOL + (z - 1) * P) * S, outb, (uint32_t)(2 * OUTR * 8));
-            if (pa + 1 < n)
-              tma_store_1d(qout + ((pa + 1) * IVOL + (z - 1) * P) * S, outb + OFFO, (uint32_t)(2 * OUTR * 8));
+            tma_store_1d(qout + (pa * IVOL + z0 * P) * S, outb, (uint32_t)(nr * OUTR * 8));
+            if (PPW == 2 && pa + 1 < n)
+              tma_store_1d(qout + ((pa + 1) * IVOL + z0 * P) * S, outb + OFFO, (uint32_t)(nr * OUTR * 8));
             bulk_commit();
           }
         }
@@ -328,15 +350,18 @@ fused2d_warp_kernel(const double* __restrict__ qin, double* __restrict__ qout, c
     }
 
     // ---- per-patch results: max wave speed (vectorized.py:226-231), redo queue ----
+    if (!act) cm = 0;
 #pragma unroll
-    for (int o = 2; o < 32; o <<= 1) {
+    for (int o = PPW; o < 32; o <<= 1) {
       const unsigned long long v = __shfl_xor_sync(0xffffffffu, cm, o);
       cm = v > cm ? v : cm;
     }
-    const unsigned sm_ = __ballot_sync(0xffffffffu, slow);
-    if (l < 2 && valid) {
+    // slot of lane l: l % PPW, both for the own volumes (slow) and the halo tasks (hslow)
+    const unsigned sm_ = __ballot_sync(0xffffffffu, (slow && act) || hslow);
+    const unsigned slot_mask = PPW == 2 ? (ps ? 0xaaaaaaaau : 0x55555555u) : 0xffffffffu;
+    if (l < PPW && pidx < n) {
       max_eig[pidx] = __longlong_as_double((long long)cm);
-      if (sm_ & (ps ? 0xaaaaaaaau : 0x55555555u)) {
+      if (sm_ & slot_mask) {
         const unsigned k = atomicAdd(&status[1], 1u);
         status[2 + k] = (unsigned)pidx;
       }
@@ -348,10 +373,12 @@ fused2d_warp_kernel(const double* __restrict__ qin, double* __restrict__ qout, c
 }  // namespace f2w
 }  // namespace fvb
 
-cudaError_t fvb_launch_fused2d16_warp(const FvbArgs& a, cudaStream_t st) {
-  using namespace fvb::f2w;
-  if (a.n <= 0) return cudaSuccess;
-  auto kfn = fused2d_warp_kernel;
+namespace fvb {
+namespace f2w {
+template <int P>
+cudaError_t launch(const FvbArgs& a, cudaStream_t st) {
+  auto kfn = fused2d_warp_kernel<P>;
+  constexpr size_t BYTES = bytes_of<P>();
   cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)BYTES);
   if (e != cudaSuccess) return e;
   int dev = 0, sms = 148;
@@ -360,11 +387,32 @@ cudaError_t fvb_launch_fused2d16_warp(const FvbArgs& a, cudaStream_t st) {
   int per_sm = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kfn, WPC * 32, BYTES);
   if (per_sm < 1) per_sm = 1;
-  const int64_t items = (a.n + 1) / 2;
+  const int64_t items = (a.n + W2<P>::PPW - 1) / W2<P>::PPW;
   int64_t grid = (int64_t)sms * per_sm;
   const int64_t need = (items + WPC - 1) / WPC;
   if (grid > need) grid = need;
-  const fvb::Closure cl{a.gamma, a.gamma - 1.0};
+  const Closure cl{a.gamma, a.gamma - 1.0};
   kfn<<<(unsigned)grid, WPC * 32, BYTES, st>>>(a.qin, a.qout, a.cell_size, a.dt, a.max_eig, a.status, a.n, cl);
   return cudaGetLastError();
+}
+}  // namespace f2w
+}  // namespace fvb
+
+// 2D patches of P = 2 .. 32 volumes per axis (AoS)
+bool fvb_fused2d_warp_supported(int p) { return p >= 2 && p <= 32; }
+
+cudaError_t fvb_launch_fused2d16_warp(const FvbArgs& a, cudaStream_t st) {
+  using namespace fvb::f2w;
+  if (a.n <= 0) return cudaSuccess;
+  switch (a.p) {
+#define FVB_P(k) \
+  case k:        \
+    return launch<k>(a, st);
+    FVB_P(2) FVB_P(3) FVB_P(4) FVB_P(5) FVB_P(6) FVB_P(7) FVB_P(8) FVB_P(9) FVB_P(10) FVB_P(11) FVB_P(12)
+    FVB_P(13) FVB_P(14) FVB_P(15) FVB_P(16) FVB_P(17) FVB_P(18) FVB_P(19) FVB_P(20) FVB_P(21) FVB_P(22)
+    FVB_P(23) FVB_P(24) FVB_P(25) FVB_P(26) FVB_P(27) FVB_P(28) FVB_P(29) FVB_P(30) FVB_P(31) FVB_P(32)
+#undef FVB_P
+    default:
+      return cudaErrorInvalidValue;
+  }
 }

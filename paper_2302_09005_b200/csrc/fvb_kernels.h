@@ -29,6 +29,7 @@ cudaError_t fvb_launch_fused3d16_half(const FvbArgs& a, cudaStream_t st);
 int fvb_fused3d_choice();
 cudaError_t fvb_launch_fused3d16_pair(const FvbArgs& a, cudaStream_t st);
 cudaError_t fvb_launch_fused2d16_warp(const FvbArgs& a, cudaStream_t st);
+bool fvb_fused2d_warp_supported(int p);
 bool fvb_fused2d_use_warp();
 cudaError_t fvb_launch_redo(const FvbArgs& a, cudaStream_t st);
 bool fvb_fused16_supported(int dim, int p, int layout);
