@@ -111,7 +111,8 @@ fused2d_warp_kernel(const double* __restrict__ qin, double* __restrict__ qout, c
 
   const int ps = PPW == 2 ? (l & 1) : 0;          // patch slot
   const int xl = PPW == 2 ? (l >> 1) : l;         // interior column of this lane
-  const bool act = xl < P;                        // lanes past the last column idle
+  constexpr bool FULL = PPW == 2 ? P == 16 : P == 32;   // every lane owns a column
+  const bool act = FULL || xl < P;                // lanes past the last column idle
   const int x = act ? xl : P - 1;                 // (addressing only)
   constexpr int LST = PPW;                        // lane step between x neighbours
   const int64_t items = (n + PPW - 1) / PPW;
@@ -212,10 +213,10 @@ fused2d_warp_kernel(const double* __restrict__ qin, double* __restrict__ qout, c
 #pragma unroll
         for (int d = 1; d < HB; ++d) {
           const int sd = s + d;
-          if (hy + d <= P) mbar_wait(&bars[sd >= NS ? sd - NS : sd], par ^ (sd >= NS ? 1u : 0u));
+          if ((P % HB == 0) || hy + d <= P) mbar_wait(&bars[sd >= NS ? sd - NS : sd], par ^ (sd >= NS ? 1u : 0u));
         }
         const int hps = l % PPW, side = (l / PPW) & 1, dr = l / (2 * PPW);
-        if (l < 2 * PPW * HB && hy + dr <= P) {
+        if (l < 2 * PPW * HB && ((P % HB == 0) || hy + dr <= P)) {
           const int sd = s + dr;
           const double* hst = ring + (sd >= NS ? sd - NS : sd) * STGD + hps * OFFB;
           double qh[S];
@@ -322,8 +323,8 @@ fused2d_warp_kernel(const double* __restrict__ qin, double* __restrict__ qout, c
           __syncwarp();
         }
         if (act) sts_q(outb + ps * OFFO + (z & 1) * OUTR + x * S, val);
-        if ((z & 1) || z == P - 1) {   // a full pair, or the last row of an odd P
-          const int nr = (z & 1) ? 2 : 1, z0 = z - (nr - 1);
+        if ((z & 1) || ((P & 1) && z == P - 1)) {   // a full pair, or the last row of an odd P
+          const int nr = ((P & 1) && !(z & 1)) ? 1 : 2, z0 = z - (nr - 1);
           fence_proxy_async();
           __syncwarp();
           if (l == 0) {
