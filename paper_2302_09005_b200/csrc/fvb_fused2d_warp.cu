@@ -33,6 +33,8 @@
 #include "fvb_layout.cuh"
 #include "fvb_tma.cuh"
 
+#include <cuda.h>
+
 namespace fvb {
 namespace f2w {
 
@@ -48,8 +50,13 @@ struct W2 {
   static constexpr int64_t VOL = (int64_t)E * E;
   static constexpr int64_t IVOL = (int64_t)P * P;
   static constexpr int ROWD = E * S;                             // doubles per haloed patch row
-  static constexpr int OFFB = (ROWD + 15) / 16 * 16 + 2;         // patch-B row offset: 16 B mod 128 B
-  static constexpr int STGD = PPW == 2 ? (OFFB + ROWD + 1) / 2 * 2 : (ROWD + 1) / 2 * 2;   // stage (16 B multiple)
+  // A stage is one TMA tensor box of [PPW patches][1 row][BOXW doubles]: the row
+  // padded by two zero-filled (out-of-bounds) doubles, so patch B's row starts
+  // 8*(ROWD+2) = 16 mod 32 bytes after patch A's (ROWD is a multiple of 4):
+  // conflict-free LDS.128 for the lane map.  One TMA op loads both patches' rows.
+  static constexpr int BOXW = ROWD + 2;
+  static constexpr int OFFB = BOXW;                              // patch-B row offset in a stage
+  static constexpr int STGD = (PPW * BOXW + 15) / 16 * 16;      // stage (tensor TMA needs 128 B alignment)
   static constexpr int NS = 7;                                   // ring stages per warp
   static constexpr int HB = 4;                                   // halo-column rows per batch
   static constexpr int XSD = 4 * 32;                             // x-side row: [c][lane]
@@ -64,7 +71,7 @@ struct W2 {
   static constexpr int W_HX = W_XS + 2 * XSD;
   static constexpr int W_OUT = W_HX + HXS;
   static constexpr int W_BAR = W_OUT + OUTD;
-  static constexpr int WARPD = (W_BAR + NS + 1) & ~1;            // doubles per warp (16 B multiple)
+  static constexpr int WARPD = (W_BAR + NS + 15) / 16 * 16;      // doubles per warp (128 B multiple)
 };
 constexpr int S = 4;
 constexpr int WPC = 4;                    // warps per CTA
@@ -93,7 +100,7 @@ template <int P>
 __global__ void __launch_bounds__(WPC * 32, 4)
 fused2d_warp_kernel(const double* __restrict__ qin, double* __restrict__ qout, const double* __restrict__ cell_size,
                     const double* __restrict__ dtv, double* __restrict__ max_eig, unsigned* __restrict__ status,
-                    int64_t n, Closure cl) {
+                    int64_t n, Closure cl, const __grid_constant__ CUtensorMap tmap) {
   using C = W2<P>;
   constexpr int E = C::E, PPW = C::PPW, ROWD = C::ROWD, OFFB = C::OFFB, STGD = C::STGD, NS = C::NS, HB = C::HB;
   constexpr int XSD = C::XSD, HXR = C::HXR, HXC = C::HXC, OUTR = C::OUTR, OFFO = C::OFFO;
@@ -126,13 +133,12 @@ fused2d_warp_kernel(const double* __restrict__ qin, double* __restrict__ qout, c
   int ij = 0, ihy = 0, is = 0, iissued = 0;
   int64_t ipa = PPW * gw;
   auto issue_next = [&]() {
-    const bool vb = PPW == 2 && ipa + 1 < n;
     double* st = ring + is * STGD;
     uint64_t* bar = bars + is;
     fence_proxy_async();
-    mbar_expect_tx(bar, (uint32_t)((vb ? 2 : 1) * ROWD * 8));
-    tma_load_1d(st, qin + (ipa * VOL + ihy * E) * S, (uint32_t)(ROWD * 8), bar);
-    if (vb) tma_load_1d(st + OFFB, qin + ((ipa + 1) * VOL + ihy * E) * S, (uint32_t)(ROWD * 8), bar);
+    // the whole box always lands (out-of-bounds elements, e.g. a missing patch B, read as zeros)
+    mbar_expect_tx(bar, (uint32_t)(PPW * C::BOXW * 8));
+    tma_load_3d(st, &tmap, 0, ihy, (int)ipa, bar);
     ++iissued;
     is = is == NS - 1 ? 0 : is + 1;
     if (++ihy == E) {
@@ -376,6 +382,39 @@ fused2d_warp_kernel(const double* __restrict__ qin, double* __restrict__ qout, c
 
 namespace fvb {
 namespace f2w {
+
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no libcuda link)
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+static EncodeTiledFn encode_tiled() {
+  static EncodeTiledFn fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(p);
+  }
+  return fn;
+}
+
+// QIn as a 3D tensor {row doubles, rows, patches}; box {row + 2 zero-filled, 1, PPW}
+template <int P>
+cudaError_t make_qin_map(const FvbArgs& a, CUtensorMap* tm) {
+  using C = W2<P>;
+  EncodeTiledFn enc = encode_tiled();
+  if (!enc) return cudaErrorNotSupported;
+  const cuuint64_t dims[3] = {(cuuint64_t)C::ROWD, (cuuint64_t)C::E, (cuuint64_t)a.n};
+  const cuuint64_t strides[2] = {(cuuint64_t)C::ROWD * 8, (cuuint64_t)C::ROWD * C::E * 8};
+  const cuuint32_t box[3] = {(cuuint32_t)C::BOXW, 1u, (cuuint32_t)C::PPW};
+  const cuuint32_t es[3] = {1u, 1u, 1u};
+  const CUresult r = enc(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double*>(a.qin), dims, strides, box, es,
+                         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
+}
+
 template <int P>
 cudaError_t launch(const FvbArgs& a, cudaStream_t st) {
   auto kfn = fused2d_warp_kernel<P>;
@@ -393,7 +432,10 @@ cudaError_t launch(const FvbArgs& a, cudaStream_t st) {
   const int64_t need = (items + WPC - 1) / WPC;
   if (grid > need) grid = need;
   const Closure cl{a.gamma, a.gamma - 1.0};
-  kfn<<<(unsigned)grid, WPC * 32, BYTES, st>>>(a.qin, a.qout, a.cell_size, a.dt, a.max_eig, a.status, a.n, cl);
+  CUtensorMap tm;
+  e = make_qin_map<P>(a, &tm);
+  if (e != cudaSuccess) return e;
+  kfn<<<(unsigned)grid, WPC * 32, BYTES, st>>>(a.qin, a.qout, a.cell_size, a.dt, a.max_eig, a.status, a.n, cl, tm);
   return cudaGetLastError();
 }
 }  // namespace f2w
