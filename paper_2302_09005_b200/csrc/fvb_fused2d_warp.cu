@@ -64,12 +64,14 @@ struct W2 {
   static constexpr int HXC = HXR * 4;                            // per component: [row slot][side][patch slot]
   static constexpr int HXS = 4 * HXC;
   static constexpr int OUTR = P * S;                             // one output row of one patch
-  static constexpr int OFFO = (2 * OUTR + 15) / 16 * 16 + 2;     // patch-B output offset: 16 B mod 128 B
-  static constexpr int OUTD = PPW == 2 ? OFFO + 2 * OUTR : 2 * OUTR;   // two rows of each patch, stored together
+  // output staging: one TMA tensor box [PPW patches][2 rows][OUTR] (dense), stored
+  // with one op every two rows; rows / patches past the tensor are not written
+  static constexpr int OFFO = 2 * OUTR;                          // patch-B offset in the staging box
+  static constexpr int OUTD = (PPW * 2 * OUTR + 15) / 16 * 16;
   static constexpr int W_RING = 0;
   static constexpr int W_XS = W_RING + NS * STGD;
   static constexpr int W_HX = W_XS + 2 * XSD;
-  static constexpr int W_OUT = W_HX + HXS;
+  static constexpr int W_OUT = (W_HX + HXS + 15) / 16 * 16;      // tensor TMA source: 128 B aligned
   static constexpr int W_BAR = W_OUT + OUTD;
   static constexpr int WARPD = (W_BAR + NS + 15) / 16 * 16;      // doubles per warp (128 B multiple)
 };
@@ -100,7 +102,8 @@ template <int P>
 __global__ void __launch_bounds__(WPC * 32, 4)
 fused2d_warp_kernel(const double* __restrict__ qin, double* __restrict__ qout, const double* __restrict__ cell_size,
                     const double* __restrict__ dtv, double* __restrict__ max_eig, unsigned* __restrict__ status,
-                    int64_t n, Closure cl, const __grid_constant__ CUtensorMap tmap) {
+                    int64_t n, Closure cl, const __grid_constant__ CUtensorMap tmap,
+                    const __grid_constant__ CUtensorMap omap) {
   using C = W2<P>;
   constexpr int E = C::E, PPW = C::PPW, ROWD = C::ROWD, OFFB = C::OFFB, STGD = C::STGD, NS = C::NS, HB = C::HB;
   constexpr int XSD = C::XSD, HXR = C::HXR, HXC = C::HXC, OUTR = C::OUTR, OFFO = C::OFFO;
@@ -330,13 +333,11 @@ fused2d_warp_kernel(const double* __restrict__ qin, double* __restrict__ qout, c
         }
         if (act) sts_q(outb + ps * OFFO + (z & 1) * OUTR + x * S, val);
         if ((z & 1) || ((P & 1) && z == P - 1)) {   // a full pair, or the last row of an odd P
-          const int nr = ((P & 1) && !(z & 1)) ? 1 : 2, z0 = z - (nr - 1);
+          const int z0 = z & ~1;   // (for odd P the box's second row is past the tensor: not written)
           fence_proxy_async();
           __syncwarp();
           if (l == 0) {
-            tma_store_1d(qout + (pa * IVOL + z0 * P) * S, outb, (uint32_t)(nr * OUTR * 8));
-            if (PPW == 2 && pa + 1 < n)
-              tma_store_1d(qout + ((pa + 1) * IVOL + z0 * P) * S, outb + OFFO, (uint32_t)(nr * OUTR * 8));
+            tma_store_3d(&omap, 0, z0, (int)pa, outb);
             bulk_commit();
           }
         }
@@ -415,6 +416,22 @@ cudaError_t make_qin_map(const FvbArgs& a, CUtensorMap* tm) {
   return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
 }
 
+// QOut as a 3D tensor {row doubles, rows, patches}; box {row, 2 rows, PPW}
+template <int P>
+cudaError_t make_qout_map(const FvbArgs& a, CUtensorMap* tm) {
+  using C = W2<P>;
+  EncodeTiledFn enc = encode_tiled();
+  if (!enc) return cudaErrorNotSupported;
+  const cuuint64_t dims[3] = {(cuuint64_t)C::OUTR, (cuuint64_t)P, (cuuint64_t)a.n};
+  const cuuint64_t strides[2] = {(cuuint64_t)C::OUTR * 8, (cuuint64_t)C::OUTR * P * 8};
+  const cuuint32_t box[3] = {(cuuint32_t)C::OUTR, 2u, (cuuint32_t)C::PPW};
+  const cuuint32_t es[3] = {1u, 1u, 1u};
+  const CUresult r = enc(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, a.qout, dims, strides, box, es,
+                         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
+}
+
 template <int P>
 cudaError_t launch(const FvbArgs& a, cudaStream_t st) {
   auto kfn = fused2d_warp_kernel<P>;
@@ -432,10 +449,12 @@ cudaError_t launch(const FvbArgs& a, cudaStream_t st) {
   const int64_t need = (items + WPC - 1) / WPC;
   if (grid > need) grid = need;
   const Closure cl{a.gamma, a.gamma - 1.0};
-  CUtensorMap tm;
+  CUtensorMap tm, om;
   e = make_qin_map<P>(a, &tm);
+  if (e == cudaSuccess) e = make_qout_map<P>(a, &om);
   if (e != cudaSuccess) return e;
-  kfn<<<(unsigned)grid, WPC * 32, BYTES, st>>>(a.qin, a.qout, a.cell_size, a.dt, a.max_eig, a.status, a.n, cl, tm);
+  kfn<<<(unsigned)grid, WPC * 32, BYTES, st>>>(a.qin, a.qout, a.cell_size, a.dt, a.max_eig, a.status, a.n, cl, tm,
+                                               om);
   return cudaGetLastError();
 }
 }  // namespace f2w
