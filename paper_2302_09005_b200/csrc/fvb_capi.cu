@@ -77,7 +77,7 @@ int fvb_update(const fvb_spec* spec, const double* qin, double* qout, const doub
   if (!qin || !qout || !cell_size || !dt || !max_eig || !status) return set_contract("null buffer");
   const int k = resolve_kernel(spec, kernel);
   if (k == FVB_KERNEL_FUSED && !fvb_fused16_supported(spec->dim, spec->p, spec->layout))
-    return set_contract("no fused kernel for this shape (2D/3D p=16, 3D p=4 AoS, 2D p=2..32 AoS)");
+    return set_contract("no fused kernel for this shape (2D/3D p=16, 3D even p=2..8 AoS, 2D p=2..32 AoS)");
   if (k != FVB_KERNEL_FUSED && k != FVB_KERNEL_GENERIC) return set_contract("unknown kernel selector");
   cudaStream_t st = as_stream(stream);
   cudaError_t e;

@@ -1,5 +1,5 @@
-// fvb_small3d.cu -- fused 3D Rusanov update for small patches (p = 4: BASELINE
-// config 4, 1M patches).
+// fvb_small3d.cu -- fused 3D Rusanov update for small patches, even p = 2 .. 8 (p = 4:
+// BASELINE config 4, 1M patches, with a tuned face-halo split).
 //
 // A persistent CTA of 64 threads processes PPC = 1 patch per iteration (one
 // thread per interior cell; 6 CTAs per SM).  The haloed patch(es) of an
@@ -41,7 +41,7 @@ struct Cfg {
   // patches per CTA iteration: 1 (64 threads, ~34 KB, 6 CTAs/SM) measured 11 % faster than
   // 2 (128 threads, 3 CTAs/SM) -- barriers over two warps, twice the independent CTAs
   static constexpr int PPC = FVB_SMALL3D_PPC;
-  static constexpr int THREADS = PPC * IVOL;
+  static constexpr int THREADS = (PPC * IVOL + 31) / 32 * 32;   // whole warps; threads past the cells idle
   static constexpr int NHALO = 6 * P * P;           // face-halo volumes per patch
   static constexpr int LINE = E * P * P;            // records of one direction: (E along n) x P x P
   static constexpr int STAGE = PPC * VOL * S;       // doubles per ring stage
@@ -88,7 +88,7 @@ __device__ __forceinline__ void put_rec(double* side, int n, int hn, int a, int 
 }
 
 template <int P>
-__global__ void __launch_bounds__(Cfg<P>::THREADS, 6 / Cfg<P>::PPC)
+__global__ void __launch_bounds__(Cfg<P>::THREADS, P == 4 ? 6 / Cfg<P>::PPC : 1)
 small3d_kernel(const double* __restrict__ qin, double* __restrict__ qout, const double* __restrict__ cell_size,
                const double* __restrict__ dtv, double* __restrict__ max_eig, unsigned* __restrict__ status,
                int64_t n_patches, Closure cl) {
@@ -110,7 +110,8 @@ small3d_kernel(const double* __restrict__ qin, double* __restrict__ qout, const 
   // (word offsets 4*hz + 5*hx mod 16 are distinct).
   const int cx = cell % P, cz = (cell / P) % P, cy = cell / (P * P);
   const int warp = tid >> 5, lane = tid & 31;
-  constexpr int WPP = C::IVOL >= 32 ? C::IVOL / 32 : 1;   // warps per patch
+  constexpr int WPP = C::THREADS / 32 / C::PPC;   // warps per patch (PPC > 1 needs IVOL % 32 == 0)
+  static_assert(C::PPC == 1 || C::IVOL % 32 == 0, "patch slots must own whole warps");
   const int64_t ngroups = (n_patches + C::PPC - 1) / C::PPC;
   const int G = ngroups > (int64_t)blockIdx.x ? (int)((ngroups - 1 - blockIdx.x) / gridDim.x + 1) : 0;
   auto group_of = [&](int g) -> int64_t { return (int64_t)blockIdx.x + (int64_t)g * gridDim.x; };
@@ -200,30 +201,38 @@ small3d_kernel(const double* __restrict__ qin, double* __restrict__ qout, const 
     // warp-uniform direction).  Warp w evaluates chunk w whole and half of chunk
     // 2*PPC + w/2, so every warp does 1.5 passes (a per-patch split would leave one
     // warp of each patch with two passes and stall the barrier).
-    {
-      static_assert(P == 4 && C::THREADS == 64 * C::PPC, "halo balancing assumes 3D p=4");
+    auto halo_eval = [&](int lpt, int nd, int hn, int a, int b) {
+      const int hx = nd == 0 ? hn : a + 1;
+      const int hy = nd == 1 ? hn : (nd == 0 ? a + 1 : b + 1);
+      const int hz = nd == 2 ? hn : b + 1;
+      const double* stt = ring + stg * C::STAGE + lpt * C::VOL * S;
+      double qh[S];
+#pragma unroll
+      for (int u = 0; u < S; ++u) qh[u] = stt[((hz * E + hy) * E + hx) * S + u];
+      Side<3> sh;
+      bool okh;
+      if (nd == 0) closure_one_ranged<3>(qh, cl, 0, sh, okh);
+      else if (nd == 1) closure_one_ranged<3>(qh, cl, 1, sh, okh);
+      else closure_one_ranged<3>(qh, cl, 2, sh, okh);
+      if (!okh) atomicOr(&slowflag[g & 1], 1u << lpt);   // rare: queue that patch for the exact pass
+      put_rec<P>(sideb + lpt * C::SIDE, nd, hn, a, b, sh);
+    };
+    if (P == 4 && C::THREADS == 64 * C::PPC) {
       auto halo_task = [&](int chunk, int idx) {
         const int lpt = chunk / 3, nd = chunk % 3;
         if (lpt >= np) return;
-        const int hn = (idx >> 4) ? E - 1 : 0;
-        const int a = idx & 3, b = (idx >> 2) & 3;   // interior coords across the face normal
-        const int hx = nd == 0 ? hn : a + 1;
-        const int hy = nd == 1 ? hn : (nd == 0 ? a + 1 : b + 1);
-        const int hz = nd == 2 ? hn : b + 1;
-        const double* stt = ring + stg * C::STAGE + lpt * C::VOL * S;
-        double qh[S];
-#pragma unroll
-        for (int u = 0; u < S; ++u) qh[u] = stt[((hz * E + hy) * E + hx) * S + u];
-        Side<3> sh;
-        bool okh;
-        if (nd == 0) closure_one_ranged<3>(qh, cl, 0, sh, okh);
-        else if (nd == 1) closure_one_ranged<3>(qh, cl, 1, sh, okh);
-        else closure_one_ranged<3>(qh, cl, 2, sh, okh);
-        if (!okh) atomicOr(&slowflag[g & 1], 1u << lpt);   // rare: queue that patch for the exact pass
-        put_rec<P>(sideb + lpt * C::SIDE, nd, hn, a, b, sh);
+        halo_eval(lpt, nd, (idx >> 4) ? E - 1 : 0, idx & 3, (idx >> 2) & 3);
       };
       halo_task(warp, lane);   // chunks 0 .. 2*PPC-1 whole, chunks 2*PPC .. 3*PPC-1 in halves
       if ((lane >> 4) == (warp & 1)) halo_task(2 * C::PPC + (warp >> 1), lane);
+    } else {
+      // other p: tasks (patch slot, face, a, b) strided over the CTA
+      for (int h = tid; h < C::PPC * C::NHALO; h += C::THREADS) {
+        const int lpt = h / C::NHALO, r = h - lpt * C::NHALO;
+        if (lpt >= np) break;
+        const int face = r / (P * P), ab = r - face * P * P;
+        halo_eval(lpt, face >> 1, (face & 1) ? E - 1 : 0, ab % P, ab / P);
+      }
     }
     if (__any_sync(0xffffffffu, slow) && lane == 0) atomicOr(&slowflag[g & 1], 1u << (lp & 31));
     if (C::NOB == 1 && tid == 0) bulk_wait_read0();   // the single staging buffer, stored last iteration, is free
@@ -330,11 +339,23 @@ cudaError_t launch(const FvbArgs& a, cudaStream_t st) {
 }  // namespace fs
 }  // namespace fvb
 
-bool fvb_small3d_supported(int dim, int p, int layout) { return dim == 3 && p == 4 && layout == fvb::kAoS; }
+// 3D AoS patches of even p = 2 .. 8 (one patch per CTA; p = 4 has the tuned halo split).
+// Odd p would make the haloed / interior patch sizes odd multiples of 8 bytes,
+// which the TMA bulk copies (16-byte granularity) cannot address per patch.
+bool fvb_small3d_supported(int dim, int p, int layout) {
+  return dim == 3 && p >= 2 && p <= 8 && (p & 1) == 0 && layout == fvb::kAoS;
+}
 
 cudaError_t fvb_launch_small3d(const FvbArgs& a, cudaStream_t st) {
   if (a.n <= 0) return cudaSuccess;
-  cudaError_t e = fvb::fs::launch<4>(a, st);
+  cudaError_t e;
+  switch (a.p) {
+    case 2: e = fvb::fs::launch<2>(a, st); break;
+    case 4: e = fvb::fs::launch<4>(a, st); break;
+    case 6: e = fvb::fs::launch<6>(a, st); break;
+    case 8: e = fvb::fs::launch<8>(a, st); break;
+    default: return cudaErrorInvalidValue;
+  }
   if (e != cudaSuccess) return e;
   return fvb_launch_redo(a, st);
 }

@@ -46,8 +46,14 @@ def test_capi_contract_checks_without_gpu():
     assert L.fvb_select_kernel(ctypes.byref(_lib.spec(3, 16, 5, 1.4))) == _lib.KERNEL_FUSED
     assert L.fvb_select_kernel(ctypes.byref(_lib.spec(3, 4, 5, 1.4))) == _lib.KERNEL_FUSED
     assert L.fvb_select_kernel(ctypes.byref(_lib.spec(3, 4, 5, 1.4, 1))) == _lib.KERNEL_GENERIC
+    assert L.fvb_select_kernel(ctypes.byref(_lib.spec(3, 6, 5, 1.4))) == _lib.KERNEL_FUSED     # even p = 2..8
     assert L.fvb_select_kernel(ctypes.byref(_lib.spec(3, 5, 5, 1.4))) == _lib.KERNEL_GENERIC
+    assert L.fvb_select_kernel(ctypes.byref(_lib.spec(3, 9, 5, 1.4))) == _lib.KERNEL_GENERIC
+    assert L.fvb_select_kernel(ctypes.byref(_lib.spec(3, 6, 5, 1.4, 1))) == _lib.KERNEL_GENERIC   # SoA
     assert L.fvb_select_kernel(ctypes.byref(_lib.spec(2, 16, 5, 1.4, 1))) == _lib.KERNEL_FUSED
+    assert L.fvb_select_kernel(ctypes.byref(_lib.spec(2, 17, 5, 1.4))) == _lib.KERNEL_FUSED     # 2D p = 2..32
+    assert L.fvb_select_kernel(ctypes.byref(_lib.spec(2, 33, 5, 1.4))) == _lib.KERNEL_GENERIC
+    assert L.fvb_select_kernel(ctypes.byref(_lib.spec(2, 17, 5, 1.4, 1))) == _lib.KERNEL_GENERIC
     assert L.fvb_update_host_workspace(ctypes.byref(_lib.spec(3, 16, 8, 1.4)), 4) > 4 * 233280 * 2
 
 
