@@ -29,10 +29,10 @@
 // reference's: -RN(c*(a-b)) equals RN(c*(b-a)) except for the sign of an
 // exact zero, which could only surface as a -0.0 result whose lower neighbour
 // holds -0.0 in that unknown (where the reference has +0.0).  Inside the range
-// gate every unknown of every evaluated volume is nonzero, and a sum that
-// starts from a nonzero value can only reach zero by exact cancellation,
-// which rounds to +0.0: a -0.0 result is impossible on the fused path.
-// Patches with zeros leave the gate and are re-evaluated by fvb_redo_kernel,
+// gate no unknown of an evaluated volume is -0.0, and a sum that starts from
+// +0.0 or a nonzero value can only reach zero as +0.0 (a sum is -0.0 only when
+// both addends are): a -0.0 result is impossible on the fused path.
+// Patches holding -0.0 leave the gate and are re-evaluated by fvb_redo_kernel,
 // which evaluates every face from both sides exactly as the reference does.
 #include <cuda_runtime.h>
 

@@ -1,4 +1,8 @@
-"""Wall time per step of driver.run_simulation on a 16^3 grid of 3D p=16 patches (4,096 patches)."""
+"""Wall time per step of driver.run_simulation on a 16^3 grid of 3D p=16 patches (4,096 patches).
+
+    python scripts/time_runsim.py          # moving fluid with a random density perturbation
+    python scripts/time_runsim.py --sod    # Sod shock tube along x: fluid at rest (exact +0 momentum)
+"""
 import sys
 import time
 
@@ -12,10 +16,16 @@ g, p = (16, 16, 16), 16
 n = int(np.prod(g))
 spec = mesh.PatchSpec(3, p, 5)
 db = device.DeviceBatch(spec, n, 1.4)
-state = torch.tensor(pde.euler_state(1.0, [0.2, 0.1, -0.1], 1.0), dtype=torch.float64, device="cuda")
 q = db.QOut.view(n, p ** 3, 5)
-q[...] = state
-q[:, :, 0] += 0.1 * torch.rand(n, p ** 3, device="cuda", dtype=torch.float64)
+if "--sod" in sys.argv:
+    left = torch.tensor(pde.euler_state(1.0, [0.0, 0.0, 0.0], 1.0), dtype=torch.float64, device="cuda")
+    right = torch.tensor(pde.euler_state(0.125, [0.0, 0.0, 0.0], 0.1), dtype=torch.float64, device="cuda")
+    px = torch.arange(n, device="cuda") % g[0]               # patch x index (x fastest)
+    q[...] = torch.where((px < g[0] // 2)[:, None, None], left, right)
+else:
+    state = torch.tensor(pde.euler_state(1.0, [0.2, 0.1, -0.1], 1.0), dtype=torch.float64, device="cuda")
+    q[...] = state
+    q[:, :, 0] += 0.1 * torch.rand(n, p ** 3, device="cuda", dtype=torch.float64)
 db.cell_size.fill_(1.0 / 16)
 driver.run_simulation(db, g, steps=2)
 torch.cuda.synchronize()
