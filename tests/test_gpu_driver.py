@@ -40,7 +40,8 @@ def test_halo_project_matches_reference(case):
     assert_bits_equal(out.cpu().numpy().reshape(gold.QIn.shape), gold.QIn, case["name"] + " soa")
 
 
-@pytest.mark.parametrize("dim,p,grid", [(3, 16, (4, 3, 2)), (2, 16, (8, 5)), (3, 4, (3, 3, 3))])
+@pytest.mark.parametrize("dim,p,grid", [(3, 16, (4, 3, 2)), (2, 16, (8, 5)), (3, 4, (3, 3, 3)), (3, 5, (1, 2, 3)),
+                                        (2, 3, (1, 1)), (2, 33, (2, 3)), (3, 2, (5, 1, 2)), (2, 17, (3, 7))])
 def test_halo_project_random_vs_oracle(dim, p, grid):
     n = int(np.prod(grid))
     b = mesh.make_patch_batch(mesh.PatchSpec(dim, p, dim + 2), n)
