@@ -144,6 +144,15 @@ int fvb_halo_project(const fvb_spec* spec, const double* qout, double* qin, cons
 size_t fvb_totals_scratch_bytes(const fvb_spec* spec);
 int fvb_totals(const fvb_spec* spec, const double* qout, double* scratch, double* totals, void* stream);
 
+/* fvb_halo_project followed by fvb_totals of the same QOut, in one pass over
+ * QOut where the batch shape allows (3D AoS, p <= 32 listed in
+ * fvb_generic.cu: the row-copy kernel sums the interior runs it moves);
+ * otherwise the two calls back to back.  The per-step loop of run_simulation
+ * (SPEC.md:446-455, :473).  The totals' summation order is deterministic for a
+ * given device but differs from fvb_totals' (both are fixed-order fp64 sums). */
+int fvb_halo_project_totals(const fvb_spec* spec, const double* qout, double* qin, const int32_t* grid_shape,
+                            int periodic, double* scratch, double* totals, void* stream);
+
 /* FVB1 batch files (host memory, no device work), byte
  * compatible with the reference's fixture dumps save_batch / load_batch
  * (mesh.py:313-353): "FVB1", int64 (d, p, s, N), then QIn, QOut,

@@ -302,6 +302,23 @@ int fvb_halo_project(const fvb_spec* spec, const double* qout, double* qin, cons
   return e == cudaSuccess ? FVB_OK : set_cuda_error(e, "fvb_halo_project");
 }
 
+int fvb_halo_project_totals(const fvb_spec* spec, const double* qout, double* qin, const int32_t* grid_shape,
+                            int periodic, double* scratch, double* totals, void* stream) {
+  int rc = check_spec(spec);
+  if (rc) return rc;
+  if (!grid_shape) return set_contract("null grid shape");
+  int64_t cells = 1;
+  for (int a = 0; a < spec->dim; ++a) {
+    if (grid_shape[a] < 1) return set_contract("grid extents must be >= 1");
+    cells *= grid_shape[a];
+  }
+  if (cells != spec->n_patches) return set_contract("grid shape does not match the patch count");
+  if (spec->n_patches == 0) return set_contract("totals over an empty batch");
+  cudaError_t e = fvb_launch_halo_project_totals(spec->dim, spec->p, spec->n_patches, spec->layout, qout, qin,
+                                                 grid_shape, periodic, scratch, totals, as_stream(stream));
+  return e == cudaSuccess ? FVB_OK : set_cuda_error(e, "fvb_halo_project_totals");
+}
+
 size_t fvb_totals_scratch_bytes(const fvb_spec* spec) {
   if (check_spec(spec)) return 0;
   return (size_t)kTotalsBlocks * spec->unknowns * sizeof(double);

@@ -384,22 +384,6 @@ fused2d_warp_kernel(const double* __restrict__ qin, double* __restrict__ qout, c
 namespace fvb {
 namespace f2w {
 
-// cuTensorMapEncodeTiled through the runtime's driver entry point (no libcuda link)
-typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
-                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
-                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
-static EncodeTiledFn encode_tiled() {
-  static EncodeTiledFn fn = nullptr;
-  if (!fn) {
-    void* p = nullptr;
-    cudaDriverEntryPointQueryResult q;
-    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
-        q == cudaDriverEntryPointSuccess)
-      fn = reinterpret_cast<EncodeTiledFn>(p);
-  }
-  return fn;
-}
-
 // QIn as a 3D tensor {row doubles, rows, patches}; box {row + 2 zero-filled, 1, PPW}
 template <int P>
 cudaError_t make_qin_map(const FvbArgs& a, CUtensorMap* tm) {

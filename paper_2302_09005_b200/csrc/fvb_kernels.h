@@ -49,7 +49,13 @@ cudaError_t fvb_launch_selftest_div(const double* a, const double* b, double* ou
                                     int64_t n, cudaStream_t st);
 cudaError_t fvb_launch_probe(int dim, double gamma, const double* states, int64_t n, double* lam, double* flux,
                              double* pressure, uint8_t* bad, cudaStream_t st);
+bool fvb_halo_tma_supported(int dim, int p);
+cudaError_t fvb_launch_halo_tma(int dim, int p, int64_t n, const double* qout, double* qin, const int* grid,
+                                int periodic, cudaStream_t st);
 cudaError_t fvb_launch_halo_project(int dim, int p, int64_t n, int layout, const double* qout, double* qin,
                                     const int* grid, int periodic, cudaStream_t st);
+cudaError_t fvb_launch_halo_project_totals(int dim, int p, int64_t n, int layout, const double* qout, double* qin,
+                                           const int* grid, int periodic, double* scratch, double* totals,
+                                           cudaStream_t st);
 cudaError_t fvb_launch_totals(int dim, int p, int64_t n, int layout, const double* qout, double* scratch,
                               double* totals, cudaStream_t st);

@@ -167,6 +167,17 @@ class DeviceBatch:
                                                 int(bool(periodic)), _stream_handle(torch, stream)),
                    "fvb_halo_project")
 
+    def halo_project_totals(self, grid_shape, periodic: bool, out, scratch, stream=None) -> None:
+        """halo_project, then out[u] <- totals of QOut (totals_into), fused into one pass where supported."""
+        from .mesh import check_grid
+
+        torch = _torch()
+        shape = check_grid(self.spec.dimensions, self.n_patches, grid_shape)
+        g = (ctypes.c_int32 * 3)(*(list(shape) + [1] * (3 - len(shape))))
+        _lib.check(_lib.load().fvb_halo_project_totals(ctypes.byref(self.fvb_spec()), _vp(self.QOut), _vp(self.QIn),
+                                                       g, int(bool(periodic)), _vp(scratch), _vp(out),
+                                                       _stream_handle(torch, stream)), "fvb_halo_project_totals")
+
     def totals_scratch(self):
         """Device scratch for totals_into (fvb_totals_scratch_bytes)."""
         torch = _torch()

@@ -148,11 +148,10 @@ def run_simulation(db: DeviceBatch, grid_shape, steps: int, cfl: float = 0.4, pe
     flag_h = torch.zeros(max(steps, 1), dtype=torch.int32, device=dev)
     scratch = db.totals_scratch()
 
-    db.halo_project(grid_shape, periodic)
+    db.halo_project_totals(grid_shape, periodic, tot_h[0], scratch)
     db.status.zero_()
     stepper = CflStepper(db, cfl=cfl, dx=dx, kernel=kernel)
     stepper.prepass()
-    db.totals_into(tot_h[0], scratch)
     gmax_h[0].copy_(stepper.gmax[0])
     for k in range(steps):
         dt_h[k].copy_(stepper.dt_scalar[0])   # the dt this step advances by
@@ -160,9 +159,8 @@ def run_simulation(db: DeviceBatch, grid_shape, steps: int, cfl: float = 0.4, pe
         db.update(kernel=kernel, zero_status=False)
         flag_h[k].copy_(db.status[0])
         stepper.reduce_dt()                   # next step's dt from this step's wave speeds
-        db.halo_project(grid_shape, periodic)
+        db.halo_project_totals(grid_shape, periodic, tot_h[k + 1], scratch)   # one pass over QOut
         gmax_h[k + 1].copy_(stepper.gmax[0])
-        db.totals_into(tot_h[k + 1], scratch)
 
     flags = flag_h.cpu().numpy()[:steps]
     bad = np.flatnonzero(flags)

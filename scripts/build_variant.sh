@@ -10,7 +10,7 @@ OUT=$ROOT/paper_2302_09005_b200/_variants
 B=$(mktemp -d)
 mkdir -p "$OUT"
 FLAGS="-gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 -fmad=false -Xcompiler -fPIC $*"
-for f in fvb_capi fvb_generic fvb_fused2d fvb_fused2d_warp fvb_fused3d fvb_fused3d_half fvb_fused3d_pair fvb_small3d; do
+for f in fvb_capi fvb_generic fvb_fused2d fvb_fused2d_warp fvb_fused3d fvb_fused3d_half fvb_fused3d_pair fvb_small3d fvb_halo_tma; do
   /usr/local/cuda/bin/nvcc $FLAGS -Xptxas -v -c "$SRC/$f.cu" -o "$B/$f.o" 2> "$B/$f.log" &
 done
 g++ -O2 -fPIC -std=c++17 -c "$SRC/fvb_io.cpp" -o "$B/fvb_io.o" &

@@ -40,8 +40,12 @@ def test_halo_project_matches_reference(case):
     assert_bits_equal(out.cpu().numpy().reshape(gold.QIn.shape), gold.QIn, case["name"] + " soa")
 
 
-@pytest.mark.parametrize("dim,p,grid", [(3, 16, (4, 3, 2)), (2, 16, (8, 5)), (3, 4, (3, 3, 3)), (3, 5, (1, 2, 3)),
-                                        (2, 3, (1, 1)), (2, 33, (2, 3)), (3, 2, (5, 1, 2)), (2, 17, (3, 7))])
+HALO_GRIDS = [(3, 16, (4, 3, 2)), (2, 16, (8, 5)), (3, 4, (3, 3, 3)), (3, 5, (1, 2, 3)), (2, 3, (1, 1)),
+              (2, 33, (2, 3)), (3, 2, (5, 1, 2)), (2, 17, (3, 7)), (3, 19, (2, 1, 2)), (2, 65, (2, 2)),
+              (3, 32, (1, 2, 1))]
+
+
+@pytest.mark.parametrize("dim,p,grid", HALO_GRIDS)
 def test_halo_project_random_vs_oracle(dim, p, grid):
     n = int(np.prod(grid))
     b = mesh.make_patch_batch(mesh.PatchSpec(dim, p, dim + 2), n)
@@ -51,6 +55,61 @@ def test_halo_project_random_vs_oracle(dim, p, grid):
         assert_bits_equal(b.QIn, oracle.halo_project(dim, p, b.QOut, grid, periodic), f"{grid} {periodic}")
     with pytest.raises(ContractViolationError):
         mesh.halo_project(b, grid[:-1], True)
+
+
+@pytest.mark.parametrize("dim,p,grid", [(3, 16, (4, 3, 2)), (3, 4, (3, 3, 3)), (3, 5, (1, 2, 3)), (2, 16, (8, 5)),
+                                        (3, 32, (1, 2, 1))])
+def test_halo_project_totals_fused(dim, p, grid):
+    """fvb_halo_project_totals: QIn bit-identical to halo_project, totals equal to an exact
+    (math.fsum) sum of QOut within fp64 summation error (the row-copy kernel sums in its own order)."""
+    import math
+
+    n = int(np.prod(grid))
+    spec = mesh.PatchSpec(dim, p, dim + 2)
+    b = mesh.make_patch_batch(spec, n)
+    b.QOut[...] = np.random.default_rng(7 * n + p).uniform(0.5, 2.0, b.QOut.shape)
+    for periodic in (True, False):
+        db = device.DeviceBatch(spec, n, 1.4)
+        db.QOut.copy_(torch.from_numpy(b.QOut.reshape(-1)))
+        tot = torch.empty(dim + 2, dtype=torch.float64, device="cuda")
+        db.halo_project_totals(grid, periodic, tot, db.totals_scratch())
+        qin = db.QIn.cpu().numpy().reshape(b.QIn.shape)
+        assert_bits_equal(qin, oracle.halo_project(dim, p, b.QOut, grid, periodic), f"{grid} {periodic}")
+        q = b.QOut.reshape(-1, dim + 2)
+        exact = np.array([math.fsum(q[:, u]) for u in range(dim + 2)])
+        np.testing.assert_allclose(tot.cpu().numpy(), exact, rtol=1e-13, atol=0)
+        np.testing.assert_allclose(db.totals(), exact, rtol=1e-13, atol=0)
+
+
+HALO_ROWS_SCRIPT = """
+import sys
+sys.path.insert(0, {root!r})
+import numpy as np
+import oracle
+from paper_2302_09005_b200 import mesh
+for dim, p, grid in {grids!r}:
+    n = int(np.prod(grid))
+    b = mesh.make_patch_batch(mesh.PatchSpec(dim, p, dim + 2), n)
+    b.QOut[...] = np.random.default_rng(n).standard_normal(b.QOut.shape)
+    for periodic in (True, False):
+        mesh.halo_project(b, grid, periodic)
+        ref = oracle.halo_project(dim, p, b.QOut, grid, periodic)
+        assert np.array_equal(b.QIn.view(np.uint64), ref.view(np.uint64)), (dim, p, grid, periodic)
+print("ok")
+"""
+
+
+def test_halo_project_thread_copy_kernels():
+    """FVB_HALO_KERNEL=rows selects the thread-copy kernels the TMA / per-patch-row paths
+    replaced (still used for shapes those do not cover); they stay bit-exact."""
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    code = HALO_ROWS_SCRIPT.format(root=root, grids=HALO_GRIDS)
+    r = subprocess.run([sys.executable, "-c", code], env={**os.environ, "FVB_HALO_KERNEL": "rows"},
+                       capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0 and r.stdout.strip().endswith("ok"), r.stdout + r.stderr
 
 
 def _db_with_field(dim, p, grid, qout):
