@@ -153,6 +153,23 @@ int fvb_totals(const fvb_spec* spec, const double* qout, double* scratch, double
 int fvb_halo_project_totals(const fvb_spec* spec, const double* qout, double* qin, const int32_t* grid_shape,
                             int periodic, double* scratch, double* totals, void* stream);
 
+/* Halo projection of one shard of a sharded grid (multi-GPU run_simulation).
+ * The shard owns whole layers of the patch grid along its slowest axis (z in
+ * 3D, y in 2D); its window is [lo_layers ghost layers from the lower
+ * neighbour | its own layers | the ghost layers from the upper neighbour],
+ * window_grid[0..dim) the window's patch counts.  qout (the shard's own QOut,
+ * spec->n_patches patches) and the ghost buffers ghost_lo / ghost_hi (interior
+ * QOut of the ghost patches, NULL when that side has none) are read; the own
+ * patches' QIn is written.  periodic_mask: bit a = wrap along axis a (x = 0);
+ * along the slowest axis a window without a ghost layer on a side clamps
+ * (zero-gradient), so a shard sets that bit only when it is the whole periodic
+ * grid.  If totals is not NULL it receives the shard's conserved totals (as
+ * fvb_halo_project_totals).  AoS, 2 <= p <= 32.  Bit-exact with
+ * fvb_halo_project of the whole grid (row f1 / §8(e)). */
+int fvb_halo_project_window(const fvb_spec* spec, const double* ghost_lo, const double* qout,
+                            const double* ghost_hi, double* qin, const int32_t* window_grid, int32_t lo_layers,
+                            int periodic_mask, double* scratch, double* totals, void* stream);
+
 /* FVB1 batch files (host memory, no device work), byte
  * compatible with the reference's fixture dumps save_batch / load_batch
  * (mesh.py:313-353): "FVB1", int64 (d, p, s, N), then QIn, QOut,

@@ -319,6 +319,35 @@ int fvb_halo_project_totals(const fvb_spec* spec, const double* qout, double* qi
   return e == cudaSuccess ? FVB_OK : set_cuda_error(e, "fvb_halo_project_totals");
 }
 
+int fvb_halo_project_window(const fvb_spec* spec, const double* ghost_lo, const double* qout,
+                            const double* ghost_hi, double* qin, const int32_t* window_grid, int32_t lo_layers,
+                            int periodic_mask, double* scratch, double* totals, void* stream) {
+  int rc = check_spec(spec);
+  if (rc) return rc;
+  if (!window_grid) return set_contract("null window grid");
+  if (spec->layout != 0) return set_contract("halo window: AoS batches only");
+  if (!fvb_halo_window_supported(spec->dim, spec->p)) return set_contract("halo window: patch size must be 2..32");
+  int64_t cells = 1, layer = 1;
+  for (int a = 0; a < spec->dim; ++a) {
+    if (window_grid[a] < 1) return set_contract("grid extents must be >= 1");
+    cells *= window_grid[a];
+    if (a < spec->dim - 1) layer *= window_grid[a];
+  }
+  if (lo_layers < 0 || spec->n_patches % layer != 0 || lo_layers * layer + spec->n_patches > cells)
+    return set_contract("own patches must be whole layers of the window");
+  if ((lo_layers > 0 && !ghost_lo) || (lo_layers * layer + spec->n_patches < cells && !ghost_hi))
+    return set_contract("missing ghost layer buffer");
+  if ((int64_t)window_grid[0] * (int64_t)spec->p * spec->p * (spec->dim == 3 ? spec->p : 1) * spec->unknowns >=
+      (1ll << 31))
+    return set_contract("halo window: x extent too large");
+  if (totals && !scratch) return set_contract("totals need the scratch buffer");
+  if (spec->n_patches == 0) return FVB_OK;
+  int g[3] = {window_grid[0], window_grid[1], spec->dim == 3 ? window_grid[2] : 1};
+  cudaError_t e = fvb_launch_halo_window(spec->dim, spec->p, spec->n_patches, ghost_lo, qout, ghost_hi, qin, g,
+                                         lo_layers, periodic_mask & 7, scratch, totals, as_stream(stream));
+  return e == cudaSuccess ? FVB_OK : set_cuda_error(e, "fvb_halo_project_window");
+}
+
 size_t fvb_totals_scratch_bytes(const fvb_spec* spec) {
   if (check_spec(spec)) return 0;
   return (size_t)kTotalsBlocks * spec->unknowns * sizeof(double);

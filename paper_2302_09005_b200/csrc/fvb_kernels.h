@@ -57,5 +57,9 @@ cudaError_t fvb_launch_halo_project(int dim, int p, int64_t n, int layout, const
 cudaError_t fvb_launch_halo_project_totals(int dim, int p, int64_t n, int layout, const double* qout, double* qin,
                                            const int* grid, int periodic, double* scratch, double* totals,
                                            cudaStream_t st);
+bool fvb_halo_window_supported(int dim, int p);
+cudaError_t fvb_launch_halo_window(int dim, int p, int64_t n, const double* ghost_lo, const double* qout,
+                                   const double* ghost_hi, double* qin, const int* window_grid, int nlo, int pmask,
+                                   double* scratch, double* totals, cudaStream_t st);
 cudaError_t fvb_launch_totals(int dim, int p, int64_t n, int layout, const double* qout, double* scratch,
                               double* totals, cudaStream_t st);

@@ -178,6 +178,18 @@ class DeviceBatch:
                                                        g, int(bool(periodic)), _vp(scratch), _vp(out),
                                                        _stream_handle(torch, stream)), "fvb_halo_project_totals")
 
+    def halo_project_window(self, window_grid, lo_layers: int, ghost_lo, ghost_hi, periodic_mask: int,
+                            totals_out=None, scratch=None, stream=None) -> None:
+        """QIn of this shard from its own QOut and the ghost layers of a sharded grid
+        (fvb_halo_project_window; driver.ShardedGrid assembles the arguments)."""
+        torch = _torch()
+        g = (ctypes.c_int32 * 3)(*(list(window_grid) + [1] * (3 - len(window_grid))))
+        _lib.check(_lib.load().fvb_halo_project_window(
+            ctypes.byref(self.fvb_spec()), _vp(ghost_lo) if ghost_lo is not None else None, _vp(self.QOut),
+            _vp(ghost_hi) if ghost_hi is not None else None, _vp(self.QIn), g, int(lo_layers), int(periodic_mask),
+            _vp(scratch) if scratch is not None else None, _vp(totals_out) if totals_out is not None else None,
+            _stream_handle(torch, stream)), "fvb_halo_project_window")
+
     def totals_scratch(self):
         """Device scratch for totals_into (fvb_totals_scratch_bytes)."""
         torch = _torch()

@@ -13,6 +13,13 @@ Per step, entirely on the device and asynchronous on one stream:
     fvb_reduce_dt(do_dt=0) local max of max_eigenvalue -> gmax (1 double)
     all_reduce(gmax, MAX)  NCCL, only when world_size > 1
     fvb_set_dt             dt = (cfl*dx)/gmax broadcast into the shard's dt[]
+
+A multi-step run over a sharded grid (run_simulation_sharded) adds the halo
+exchange: each rank owns whole layers of the patch grid along its slowest axis
+and swaps one boundary layer of interior QOut with each neighbour (NCCL
+send/recv over NVLink), then rebuilds its QIn from its own layers and the two
+ghost layers (fvb_halo_project_window), bit-identical to the single-GPU
+halo_project of the whole grid.
 """
 
 from __future__ import annotations
@@ -172,4 +179,163 @@ def run_simulation(db: DeviceBatch, grid_shape, steps: int, cfl: float = 0.4, pe
     res.t = [0.0] + [float(v) for v in np.cumsum(res.dt)]
     res.max_eigenvalue = [float(v) for v in gmax_h.cpu().numpy()]
     res.totals = list(tot_h.cpu().numpy())
+    return res
+
+
+# --- sharded grid: ghost-layer exchange + windowed halo projection (multi-GPU run_simulation) ---------
+
+
+def _neighbours(rank: int, world: int, periodic: bool):
+    """(lower, upper) neighbour ranks along the sharded axis; None at a non-periodic edge."""
+    lo = rank - 1 if rank > 0 else (world - 1 if periodic else None)
+    hi = rank + 1 if rank < world - 1 else (0 if periodic else None)
+    return lo, hi
+
+
+def exchange_ghost_layers(own, layer_elems: int, ghost_lo, ghost_hi, rank: int, world: int, periodic: bool,
+                          group=None) -> None:
+    """Fill ghost_lo with the lower neighbour's last layer and ghost_hi with the upper
+    neighbour's first layer (flat tensors; `own` holds whole layers of layer_elems values).
+
+    Point-to-point sends / receives (NCCL over NVLink on GPU ranks, any backend on CPU),
+    issued in one fixed order on every rank -- [send last -> upper, send first -> lower,
+    recv lower, recv upper] -- so that with two ranks, where the lower and upper
+    neighbour are the same rank, the k-th message between a pair still lands in the
+    right buffer.  A single periodic rank copies its own layers."""
+    lo, hi = _neighbours(rank, world, periodic)
+    first, last = own[:layer_elems], own[own.numel() - layer_elems:]
+    if world == 1:
+        if lo is not None:
+            ghost_lo.copy_(last)
+        if hi is not None:
+            ghost_hi.copy_(first)
+        return
+    import torch.distributed as dist
+
+    ops = []
+    if hi is not None:
+        ops.append(dist.P2POp(dist.isend, last.contiguous(), hi, group))
+    if lo is not None:
+        ops.append(dist.P2POp(dist.isend, first.contiguous(), lo, group))
+    if lo is not None:
+        ops.append(dist.P2POp(dist.irecv, ghost_lo, lo, group))
+    if hi is not None:
+        ops.append(dist.P2POp(dist.irecv, ghost_hi, hi, group))
+    for w in dist.batch_isend_irecv(ops):
+        w.wait()
+
+
+class ShardedGrid:
+    """One rank's shard of a logical uniform patch grid, split in whole layers along the
+    slowest axis (z in 3D, y in 2D; patch index x-fastest as in halo_project).
+
+    db is the rank's DeviceBatch (its own patches, global order); ghost_lo / ghost_hi
+    hold the neighbours' boundary layers of interior QOut.  halo() exchanges them and
+    rebuilds db.QIn exactly as halo_project of the whole grid would."""
+
+    def __init__(self, spec, grid_shape, gamma: float, periodic: bool = True, rank: int | None = None,
+                 world: int | None = None, group=None, device=None):
+        import torch.distributed as dist
+
+        torch = _torch()
+        self.grid = tuple(int(g) for g in grid_shape)
+        d = spec.dimensions
+        if len(self.grid) != d:
+            from .errors import ContractViolationError
+            raise ContractViolationError(f"grid shape {self.grid} has {len(self.grid)} axes, expected {d}")
+        on = dist.is_available() and dist.is_initialized()
+        self.rank = rank if rank is not None else (dist.get_rank(group) if on else 0)
+        self.world = world if world is not None else (dist.get_world_size(group) if on else 1)
+        self.group, self.periodic = group, bool(periodic)
+        layer = 1
+        for g in self.grid[:-1]:
+            layer *= g
+        self.layer = layer
+        if self.grid[-1] < self.world:
+            from .errors import ContractViolationError
+            raise ContractViolationError(f"{self.world} ranks need at least {self.world} layers along the sharded "
+                                         f"axis, grid {self.grid} has {self.grid[-1]}")
+        self.l0, self.l1 = shard_bounds(self.grid[-1], self.rank, self.world)
+        self.patch_lo, self.patch_hi = self.l0 * layer, self.l1 * layer
+        n_own = self.patch_hi - self.patch_lo
+        self.db = DeviceBatch(spec, n_own, gamma, device)
+        self.layer_elems = layer * spec.interior_volumes * spec.unknowns
+        lo, hi = _neighbours(self.rank, self.world, self.periodic)
+        f64 = dict(dtype=torch.float64, device=self.db.device)
+        self.ghost_lo = torch.empty(self.layer_elems, **f64) if lo is not None else None
+        self.ghost_hi = torch.empty(self.layer_elems, **f64) if hi is not None else None
+        self.lo_layers = 1 if lo is not None else 0
+        own_layers = self.l1 - self.l0
+        self.window_grid = self.grid[:-1] + (self.lo_layers + own_layers + (1 if hi is not None else 0),)
+        # wrap along x / y (3D) or x (2D); the sharded axis wraps through the ghost layers
+        self.pmask = ((1 << (d - 1)) - 1) if self.periodic else 0
+
+    def exchange(self) -> None:
+        exchange_ghost_layers(self.db.QOut, self.layer_elems, self.ghost_lo, self.ghost_hi, self.rank, self.world,
+                              self.periodic, self.group)
+
+    def halo(self, totals_out=None, scratch=None) -> None:
+        """Ghost exchange, then this shard's QIn (and its local totals if totals_out is given)."""
+        self.exchange()
+        self.db.halo_project_window(self.window_grid, self.lo_layers, self.ghost_lo, self.ghost_hi, self.pmask,
+                                    totals_out, scratch)
+
+
+def run_simulation_sharded(sg: ShardedGrid, steps: int, cfl: float = 0.4, kernel="auto",
+                           dx: float | None = None) -> SimulationResult:
+    """run_simulation over a grid sharded across ranks (one GPU each): the same step --
+    dt from the global maximum wave speed (one MAX all-reduce), fused update of the own
+    patches, then the ghost-layer exchange and the windowed halo projection.  Totals are
+    summed over ranks in rank order.  With one rank it reproduces run_simulation bit for bit
+    (the exchange is a local copy)."""
+    import numpy as np
+    import torch.distributed as dist
+
+    torch = _torch()
+    db = sg.db
+    s = db.spec.unknowns
+    f64 = dict(dtype=torch.float64, device=db.device)
+    tot_h = torch.empty((steps + 1, s), **f64)
+    gmax_h = torch.empty(steps + 1, **f64)
+    dt_h = torch.empty(max(steps, 1), **f64)
+    flag_h = torch.zeros(max(steps, 1), dtype=torch.int32, device=db.device)
+    scratch = db.totals_scratch()
+    multi = sg.world > 1
+
+    def halo_and_totals(k):
+        sg.halo(tot_h[k], scratch)
+        if multi:   # global totals: gather the shards' vectors, sum in rank order (deterministic)
+            parts = [torch.empty(s, **f64) for _ in range(sg.world)]
+            dist.all_gather(parts, tot_h[k].contiguous(), group=sg.group)
+            acc = parts[0].clone()
+            for t in parts[1:]:
+                acc += t
+            tot_h[k].copy_(acc)
+
+    halo_and_totals(0)
+    db.status.zero_()
+    stepper = CflStepper(db, cfl=cfl, dx=dx, kernel=kernel, group=sg.group)
+    stepper.prepass()
+    gmax_h[0].copy_(stepper.gmax[0])
+    for k in range(steps):
+        dt_h[k].copy_(stepper.dt_scalar[0])
+        db.status[1:2].zero_()
+        db.update(kernel=kernel, zero_status=False)
+        flag_h[k].copy_(db.status[0])
+        stepper.reduce_dt()
+        halo_and_totals(k + 1)
+        gmax_h[k + 1].copy_(stepper.gmax[0])
+
+    flags = flag_h.clone()
+    if multi:
+        dist.all_reduce(flags, op=dist.ReduceOp.MAX, group=sg.group)
+    bad = np.flatnonzero(flags.cpu().numpy()[:steps])
+    if bad.size:
+        from .errors import NonPhysicalStateError
+        raise NonPhysicalStateError("non-physical state during run_simulation", step=int(bad[0]))
+    res = SimulationResult(db.spec.dimensions)
+    res.dt = [float(v) for v in dt_h.cpu().numpy()[:steps]]
+    res.t = [0.0] + [float(v) for v in np.cumsum(res.dt)]
+    res.max_eigenvalue = [float(v) for v in gmax_h.cpu().numpy()]
+    res.totals = [row for row in tot_h.cpu().numpy()]
     return res

@@ -185,3 +185,65 @@ def test_run_simulation_convergence_order():
         errors.append(float(np.abs(out[..., 0] - exact).mean()))
     orders = [np.log(errors[k] / errors[k + 1]) / np.log(3.0) for k in range(2)]
     assert min(orders) >= 0.7, (errors, orders)
+
+
+@pytest.mark.parametrize("dim,p,grid", [(3, 16, (3, 2, 5)), (3, 5, (2, 3, 4)), (2, 16, (4, 7)), (2, 17, (3, 3)),
+                                        (3, 4, (2, 2, 1))])
+@pytest.mark.parametrize("world", [1, 2, 3])
+def test_sharded_halo_window_matches_global(dim, p, grid, world):
+    """fvb_halo_project_window on each shard of a grid split in whole layers along its slowest
+    axis, ghosts filled with the neighbours' boundary layers, equals the single-GPU halo
+    projection of the whole grid bit for bit (periodic and zero-gradient); the shards' totals
+    sum to the whole grid's."""
+    import math
+
+    n = int(np.prod(grid))
+    spec = mesh.PatchSpec(dim, p, dim + 2)
+    if grid[-1] < world:   # every rank must own a layer
+        with pytest.raises(ContractViolationError):
+            driver.ShardedGrid(spec, grid, 1.4, True, rank=0, world=world)
+        return
+    qout = np.random.default_rng(n + 31 * p + world).uniform(0.5, 2.0, (n, p ** dim * (dim + 2)))
+    layer = n // grid[-1]
+    le = layer * p ** dim * (dim + 2)
+    for periodic in (True, False):
+        ref = oracle.halo_project(dim, p, qout, grid, periodic).reshape(n, -1)
+        tot_sum = np.zeros(dim + 2)
+        for rank in range(world):
+            sg = driver.ShardedGrid(spec, grid, 1.4, periodic, rank=rank, world=world)
+            sg.db.QOut.copy_(torch.from_numpy(qout[sg.patch_lo:sg.patch_hi].reshape(-1).copy()))
+            flat = qout.reshape(-1)
+            if sg.ghost_lo is not None:   # the lower neighbour's last layer (wrapping)
+                z = (sg.l0 - 1) % grid[-1]
+                sg.ghost_lo.copy_(torch.from_numpy(flat[z * le:(z + 1) * le].copy()))
+            if sg.ghost_hi is not None:
+                z = sg.l1 % grid[-1]
+                sg.ghost_hi.copy_(torch.from_numpy(flat[z * le:(z + 1) * le].copy()))
+            tot = torch.empty(dim + 2, dtype=torch.float64, device="cuda")
+            sg.db.halo_project_window(sg.window_grid, sg.lo_layers, sg.ghost_lo, sg.ghost_hi, sg.pmask, tot,
+                                      sg.db.totals_scratch())
+            got = sg.db.QIn.cpu().numpy().reshape(sg.db.n_patches, -1)
+            assert_bits_equal(got, ref[sg.patch_lo:sg.patch_hi], f"rank {rank}/{world} periodic={periodic}")
+            tot_sum += tot.cpu().numpy()
+        exact = np.array([math.fsum(qout.reshape(-1, dim + 2)[:, u]) for u in range(dim + 2)])
+        np.testing.assert_allclose(tot_sum, exact, rtol=1e-13)
+
+
+@pytest.mark.parametrize("dim,p,grid", [(3, 16, (2, 2, 3)), (2, 16, (4, 5))])
+@pytest.mark.parametrize("periodic", [True, False])
+def test_run_simulation_sharded_single_rank_matches(dim, p, grid, periodic):
+    """run_simulation_sharded with one rank (the exchange is a local copy) reproduces
+    run_simulation bit for bit: QOut and the dt history (totals to summation-order rounding:
+    2D run_simulation sums them in a separate pass)."""
+    n = int(np.prod(grid))
+    q = oracle.synthetic_qin(dim, p, n, seed=12).reshape(n, (p + 2) ** dim, dim + 2)
+    sl = (slice(None),) + (slice(1, -1),) * dim + (slice(None),)
+    interior = q.reshape((n,) + (p + 2,) * dim + (dim + 2,))[sl].reshape(n, -1)
+    db = _db_with_field(dim, p, grid, interior)
+    ref = driver.run_simulation(db, grid, steps=6, cfl=0.4, periodic=periodic)
+    sg = driver.ShardedGrid(mesh.PatchSpec(dim, p, dim + 2), grid, 1.4, periodic, rank=0, world=1)
+    sg.db.QOut.copy_(torch.from_numpy(interior.reshape(-1).copy()))
+    res = driver.run_simulation_sharded(sg, steps=6, cfl=0.4)
+    assert_bits_equal(sg.db.QOut.cpu().numpy(), db.QOut.cpu().numpy(), "QOut after 6 steps")
+    assert res.dt == ref.dt
+    np.testing.assert_allclose(np.asarray(res.totals), np.asarray(ref.totals), rtol=1e-13)
