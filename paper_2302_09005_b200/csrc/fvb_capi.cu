@@ -350,7 +350,7 @@ int fvb_halo_project_window(const fvb_spec* spec, const double* ghost_lo, const 
 
 size_t fvb_totals_scratch_bytes(const fvb_spec* spec) {
   if (check_spec(spec)) return 0;
-  return (size_t)kTotalsBlocks * spec->unknowns * sizeof(double);
+  return (size_t)kScratchBlocks * spec->unknowns * sizeof(double);
 }
 
 int fvb_totals(const fvb_spec* spec, const double* qout, double* scratch, double* totals, void* stream) {

@@ -9,6 +9,7 @@ struct BoxInfo {
 };
 
 constexpr int kTotalsBlocks = 592;   // partial-sum blocks of fvb_totals (scratch = blocks x unknowns doubles)
+constexpr int kScratchBlocks = 2048;  // scratch partials available (fvb_totals_scratch_bytes): also the halo CTAs
 
 struct FvbArgs {
   int dim, p, layout;
