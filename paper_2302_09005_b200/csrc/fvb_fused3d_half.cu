@@ -65,7 +65,18 @@ constexpr int OFF_WMAX = OFF_OUT + 2 * OUTN;
 constexpr int OFF_FLAG = OFF_WMAX + 8;
 constexpr int OFF_TMEM = OFF_FLAG + 1;    // TMEM base address (4 B) + padding
 constexpr int OFF_BAR = OFF_TMEM + 1;
-constexpr int TOTAL = OFF_BAR + NST;
+#ifndef FVB3D_SYNC
+#define FVB3D_SYNC 0
+#endif
+// FVB3D_SYNC = 1: instead of one CTA barrier per plane, per-warp mbarriers by
+// buffer parity -- F[w][p] "warp w published its side data of a plane of parity
+// p" and E[w][p] "interior warp w finished updating from parity-p data" -- so a
+// warp waits only for the warps whose rows it reads (its y neighbours and the
+// halo warp) instead of the slowest warp of the CTA.
+constexpr bool SPLIT_SYNC = FVB3D_SYNC != 0;
+constexpr int OFF_FBAR = OFF_BAR + NST;               // F[NIW + 1][2]
+constexpr int OFF_EBAR = OFF_FBAR + 2 * (NIW + 1);    // E[NIW][2]
+constexpr int TOTAL = OFF_EBAR + 2 * NIW;
 constexpr size_t BYTES = (size_t)TOTAL * 8;
 #ifndef FVB3D_OWN_TMEM
 #define FVB3D_OWN_TMEM 0
@@ -202,9 +213,15 @@ fused3d_half_kernel(const double* __restrict__ qin, double* __restrict__ qout, c
     }
   };
 
+  uint64_t* fbar = reinterpret_cast<uint64_t*>(sm + OFF_FBAR);
+  uint64_t* ebar = reinterpret_cast<uint64_t*>(sm + OFF_EBAR);
   if (producer) {
 #pragma unroll
     for (int s = 0; s < NST; ++s) mbar_init(&bars[s], 1);
+    if (SPLIT_SYNC) {
+      for (int b = 0; b < 2 * (NIW + 1); ++b) mbar_init(&fbar[b], 1);
+      for (int b = 0; b < 2 * NIW; ++b) mbar_init(&ebar[b], 1);
+    }
     slowflag[0] = slowflag[1] = 0;
     fence_mbar_init();
   }
@@ -219,6 +236,10 @@ fused3d_half_kernel(const double* __restrict__ qin, double* __restrict__ qout, c
     issue(0, 1, 1);
   }
 
+#ifdef FVB3D_PROFILE_BARRIER
+  long long work_cycles = 0, wait_cycles = 0;
+  const long long t_start = clock64();
+#endif
   bool slow = false;
   unsigned long long cm = 0;
   Side<3> zprev;
@@ -245,6 +266,13 @@ fused3d_half_kernel(const double* __restrict__ qin, double* __restrict__ qout, c
 
     auto plane = [&](int zh, auto kind) {
       constexpr int K = decltype(kind)::value;
+      // split sync: iteration g (global plane count) arrives on parity g & 1, completing
+      // that barrier's phase g >> 1
+      const int g = jp * NPL + zh;
+      const unsigned pa = (unsigned)(g & 1);
+      const unsigned ph_prev = (unsigned)(((g - 1) >> 1) & 1), ph_cur = (unsigned)((g >> 1) & 1);
+      auto wait_e_prev = [&](int w) { mbar_wait(&ebar[2 * w + (pa ^ 1u)], ph_prev); };   // B(g-1) of warp w done
+      auto wait_f_prev = [&](int w) { mbar_wait(&fbar[2 * w + (pa ^ 1u)], ph_prev); };   // A(g-1) of warp w done
       const unsigned stg = (unsigned)(zh % NST), par = (unsigned)((zh / NST) & 1);
       const unsigned stp = stg == 0 ? NST - 1 : stg - 1;   // stage of plane zh-1
       const double* st = ring + stg * STAGE;
@@ -253,10 +281,21 @@ fused3d_half_kernel(const double* __restrict__ qin, double* __restrict__ qout, c
       double* xs_w = xsb + (zh & 1) * XS;
       const double* ys_r = ysb + ((zh - 1) & 1) * YS;
       const double* xs_r = xsb + ((zh - 1) & 1) * XS;
+#ifdef FVB3D_PROFILE_BARRIER
+      const long long tw0 = clock64();
       mbar_wait(&bars[stg], par);
+      const long long tw1 = clock64();
+      wait_cycles += tw1 - tw0;
+#else
+      mbar_wait(&bars[stg], par);
+#endif
 
       if (interior) {
         if (OWN_TMEM) tmem_wait_st();   // last iteration's record (read below) has landed
+        if (SPLIT_SYNC && g >= 1) {     // WAR: A(g) overwrites what B(g-1) of the y neighbours read
+          if (warp > 0) wait_e_prev(warp - 1);
+          if (warp < NIW - 1) wait_e_prev(warp + 1);
+        }
         Side<3> zcur;
         double q[S];
         load_q<L>(st, ly + 1, x + 1, q);
@@ -298,7 +337,16 @@ fused3d_half_kernel(const double* __restrict__ qin, double* __restrict__ qout, c
             favg_zm[u] = dadd(c, u == 0 ? q[3] : zcur.f[u - 1]);
           }
         }
+        if (SPLIT_SYNC) {   // A(g) published
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&fbar[2 * warp + pa]);
+        }
         if (K == kSteady || K == kZHi) {
+          if (SPLIT_SYNC) {   // RAW: B(g) reads the y neighbours' and the halo warp's A(g-1)
+            wait_f_prev(warp > 0 ? warp - 1 : NIW);
+            wait_f_prev(warp < NIW - 1 ? warp + 1 : NIW);
+            if (warp > 0 && warp < NIW - 1) wait_f_prev(NIW);
+          }
           double qc[S], val[S], qn[S], ra[8], rb[8];
           double lx, lyv;
           if (OWN_TMEM) {
@@ -372,6 +420,10 @@ fused3d_half_kernel(const double* __restrict__ qin, double* __restrict__ qout, c
         // the halo warp: stage rows 0 and 9 (y-face halo row and the ghost row
         // of the other half) need y-side data; interior rows need the x-face
         // halo columns' x-side data
+        if (SPLIT_SYNC && g >= 1) {   // WAR: every interior warp's B(g-1) read these buffers
+#pragma unroll
+          for (int w = 0; w < NIW; ++w) wait_e_prev(w);
+        }
         {
           const int r = lane < 16 ? 0 : SR - 1;
           double qh[S];
@@ -410,14 +462,29 @@ fused3d_half_kernel(const double* __restrict__ qin, double* __restrict__ qout, c
           cm = 0;
         }
       }
-      if (producer) bulk_wait_read0();
-      __syncthreads();
+      if (SPLIT_SYNC) {
+        __syncwarp();
+        if (lane == 0) mbar_arrive(interior ? &ebar[2 * warp + pa] : &fbar[2 * NIW + pa]);
+        if (producer) {   // the ring stage and the output buffer of this plane: after every B(g)
+#pragma unroll
+          for (int w = 0; w < NIW; ++w) mbar_wait(&ebar[2 * w + pa], ph_cur);
+        }
+      } else {
+        if (producer) bulk_wait_read0();
+#ifdef FVB3D_PROFILE_BARRIER
+        work_cycles += clock64() - tw1;   // from the ring wait to the barrier: this warp's work
+#endif
+        __syncthreads();
+      }
       if (producer) {
         const int zn = zh + 2 < NPL ? zh + 2 : zh + 2 - NPL;
         const int jn = zh + 2 < NPL ? jp : jp + 1;
         if (jn < my_items) issue(jn, zn, stp);
         if (K == kSteady || K == kZHi) store_out(pidx, y0, zh - 2);
         if (K == kZHi) finish_item(jp, pidx);
+        // split sync: the next B into this output buffer (iteration g+2) waits for the
+        // halo warp's A(g+1), which this thread reaches only after the store read it
+        if (SPLIT_SYNC) bulk_wait_read0();
       }
     };
 
@@ -434,6 +501,16 @@ fused3d_half_kernel(const double* __restrict__ qin, double* __restrict__ qout, c
     if (warp == 0) tmem_dealloc(*tmem_slot, TMEM_COLS);
   }
   if (producer) bulk_wait_all0();
+#ifdef FVB3D_PROFILE_BARRIER
+  // diagnostic build only: per-role barrier cycles / total cycles, accumulated into
+  // the (otherwise unused here) tail of the status buffer's redo list
+  if (lane == 0) {
+    unsigned long long* acc = reinterpret_cast<unsigned long long*>(status + 2 + 2 * n + 64);
+    atomicAdd(acc + (interior ? 0 : 3), (unsigned long long)work_cycles);
+    atomicAdd(acc + (interior ? 1 : 4), (unsigned long long)wait_cycles);
+    atomicAdd(acc + (interior ? 2 : 5), (unsigned long long)(clock64() - t_start));
+  }
+#endif
 }
 
 template <int L>
