@@ -17,6 +17,8 @@
 #include <cuda_runtime.h>
 
 #include "fvb_exact.cuh"
+#include <cstring>
+
 #include "fvb_kernels.h"
 #include "fvb_layout.cuh"
 #include "fvb_tma.cuh"
@@ -47,10 +49,10 @@ struct Cfg {
   static constexpr int STAGE = PPC * VOL * S;       // doubles per ring stage
   static constexpr int NST = 2;
   static constexpr int SIDE = 3 * S * LINE;         // side data of one patch, 3 directions
-  static constexpr int OUTN = PPC * IVOL * S;
+  static constexpr int OUTN = (PPC * IVOL * S + 15) / 16 * 16;   // staging buffers 128-byte aligned (TMA)
   static constexpr int OFF_RING = 0;
   static constexpr int OFF_SIDE = OFF_RING + NST * STAGE;
-  static constexpr int OFF_OUT = OFF_SIDE + PPC * SIDE;
+  static constexpr int OFF_OUT = (OFF_SIDE + PPC * SIDE + 15) / 16 * 16;
   // output staging: NOB buffers (1: the store of iteration g-1 must have read it
   // before phase B of iteration g writes; checked before the mid-iteration barrier)
   static constexpr int NOB = FVB_SMALL3D_NOB;
@@ -87,11 +89,25 @@ __device__ __forceinline__ void put_rec(double* side, int n, int hn, int a, int 
   for (int k = 0; k < 4; ++k) side[side_at<P>(n, k + 1, hn, a, b)] = s.f[k];
 }
 
+// Output staging order.  The thread mapping puts (x, z) in a half-warp, for which
+// the AoS interior order (x, y, z) makes the z step a multiple of 16 doubles: the
+// five STS.64 per cell would be 4-way bank-conflicted (ncu: 4x the ideal
+// wavefronts at p = 4).  The staging is therefore (x, z, y) -- word offsets
+// 5x + 4z mod 16 distinct at p = 4 -- and one tiled TMA store whose tensor map
+// walks QOut as {x*S, z, y, patch} writes it back in AoS order.
+#ifndef FVB_SMALL3D_TOUT
+#define FVB_SMALL3D_TOUT 1
+#endif
+constexpr bool TOUT = FVB_SMALL3D_TOUT != 0;
+#ifndef FVB_SMALL3D_REMAP
+#define FVB_SMALL3D_REMAP 1
+#endif
+
 template <int P>
 __global__ void __launch_bounds__(Cfg<P>::THREADS, P == 4 ? 6 / Cfg<P>::PPC : 1)
 small3d_kernel(const double* __restrict__ qin, double* __restrict__ qout, const double* __restrict__ cell_size,
                const double* __restrict__ dtv, double* __restrict__ max_eig, unsigned* __restrict__ status,
-               int64_t n_patches, Closure cl) {
+               int64_t n_patches, Closure cl, const __grid_constant__ CUtensorMap omap) {
   using C = Cfg<P>;
   constexpr int S = C::S, E = C::E;
   extern __shared__ __align__(128) double sm[];
@@ -218,10 +234,33 @@ small3d_kernel(const double* __restrict__ qin, double* __restrict__ qout, const 
       put_rec<P>(sideb + lpt * C::SIDE, nd, hn, a, b, sh);
     };
     if (P == 4 && C::THREADS == 64 * C::PPC) {
+      // task idx -> (face side h, a, b), chosen per direction so that a half-warp's
+      // stage loads and record stores hit distinct bank pairs where possible:
+      //   x faces: a in {0,1} / {2,3} per half-warp, h, b      (loads and stores)
+      //   y faces: a, b, h per half-warp                        (loads and stores)
+      //   z faces: a, h, b in {0,1} / {2,3} per half-warp       (stores; loads 2 pairs 2-way)
       auto halo_task = [&](int chunk, int idx) {
         const int lpt = chunk / 3, nd = chunk % 3;
         if (lpt >= np) return;
-        halo_eval(lpt, nd, (idx >> 4) ? E - 1 : 0, idx & 3, (idx >> 2) & 3);
+        int h, a, b;
+        if (!FVB_SMALL3D_REMAP) {
+          a = idx & 3;
+          b = (idx >> 2) & 3;
+          h = idx >> 4;
+        } else if (nd == 0) {
+          a = (idx & 1) | ((idx >> 4) << 1);
+          h = (idx >> 1) & 1;
+          b = (idx >> 2) & 3;
+        } else if (nd == 1) {
+          a = idx & 3;
+          b = (idx >> 2) & 3;
+          h = idx >> 4;
+        } else {
+          a = idx & 3;
+          h = (idx >> 2) & 1;
+          b = ((idx >> 3) & 1) | ((idx >> 4) << 1);
+        }
+        halo_eval(lpt, nd, h ? E - 1 : 0, a, b);
       };
       halo_task(warp, lane);   // chunks 0 .. 2*PPC-1 whole, chunks 2*PPC .. 3*PPC-1 in halves
       if ((lane >> 4) == (warp & 1)) halo_task(2 * C::PPC + (warp >> 1), lane);
@@ -274,7 +313,8 @@ small3d_kernel(const double* __restrict__ qin, double* __restrict__ qout, const 
           val[u] = dadd(val[u], dmul(half_inv, dsub(dadd(fm, fc), dadd(fc, fp))));
         }
       }
-      const int lin = (cz * P + cy) * P + cx;   // AoS interior order (x fastest)
+      const int lin = TOUT ? (cy * P + cz) * P + cx    // staging order (x, z, y), see TOUT
+                           : (cz * P + cy) * P + cx;   // AoS interior order (x fastest)
 #pragma unroll
       for (int u = 0; u < S; ++u) outb[(g % C::NOB) * C::OUTN + (lp * C::IVOL + lin) * S + u] = val[u];
       fence_proxy_async();
@@ -290,8 +330,11 @@ small3d_kernel(const double* __restrict__ qin, double* __restrict__ qout, const 
     __syncthreads();
     if (tid == 0) {
       // output of this group, per-patch maxima, redo list; then refill the freed stage
-      tma_store_1d(qout + grp * C::PPC * (int64_t)C::IVOL * S, outb + (g % C::NOB) * C::OUTN,
-                   (uint32_t)(np * C::IVOL * S * 8));
+      if (TOUT)
+        tma_store_4d(&omap, 0, 0, 0, (int)(grp * C::PPC), outb + (g % C::NOB) * C::OUTN);
+      else
+        tma_store_1d(qout + grp * C::PPC * (int64_t)C::IVOL * S, outb + (g % C::NOB) * C::OUTN,
+                     (uint32_t)(np * C::IVOL * S * 8));
       bulk_commit();
       const unsigned flags = slowflag[g & 1];
       for (int k = 0; k < np; ++k) {
@@ -331,8 +374,23 @@ cudaError_t launch(const FvbArgs& a, cudaStream_t st) {
   int64_t grid = (int64_t)sms * per_sm;
   if (grid > groups) grid = groups;
   const Closure cl{a.gamma, a.gamma - 1.0};
+  CUtensorMap omap;
+  memset(&omap, 0, sizeof(omap));
+  if (TOUT) {   // QOut as {x*S, z, y, patch}: the staging's (x, z, y) order, AoS in memory
+    EncodeTiledFn enc = encode_tiled();
+    if (!enc) return cudaErrorNotSupported;
+    const cuuint64_t dims[4] = {(cuuint64_t)P * C::S, (cuuint64_t)P, (cuuint64_t)P, (cuuint64_t)a.n};
+    const cuuint64_t strides[3] = {(cuuint64_t)P * P * C::S * 8, (cuuint64_t)P * C::S * 8,
+                                   (cuuint64_t)C::IVOL * C::S * 8};
+    const cuuint32_t box[4] = {(cuuint32_t)(P * C::S), (cuuint32_t)P, (cuuint32_t)P, (cuuint32_t)C::PPC};
+    const cuuint32_t es[4] = {1u, 1u, 1u, 1u};
+    if (enc(&omap, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, a.qout, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+            CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) !=
+        CUDA_SUCCESS)
+      return cudaErrorInvalidValue;
+  }
   kfn<<<(unsigned)grid, C::THREADS, C::BYTES, st>>>(a.qin, a.qout, a.cell_size, a.dt, a.max_eig, a.status, a.n,
-                                                    cl);
+                                                    cl, omap);
   return cudaGetLastError();
 }
 
