@@ -170,6 +170,27 @@ int fvb_halo_project_window(const fvb_spec* spec, const double* ghost_lo, const 
                             const double* ghost_hi, double* qin, const int32_t* window_grid, int32_t lo_layers,
                             int periodic_mask, double* scratch, double* totals, void* stream);
 
+/* Multi-GPU: the step's single exchange, a MAX all-reduce of the global wave
+ * speed (one fp64) over NCCL on NVLink / NVSwitch (the
+ * ncclAllReduce of the north star), for hosts that do not use torch.distributed.
+ * NCCL is dlopen'ed ("libnccl.so.2") on first use.
+ *   One process, ndev GPUs:   fvb_mgpu_init(ndev, devs) (ncclCommInitAll), then per
+ *     step fvb_mgpu_allreduce_max_all(bufs, streams) (one NCCL group over all
+ *     ranks) or fvb_mgpu_allreduce_max(rank, buf, stream) from one thread per GPU.
+ *   One process per GPU:      rank 0 calls fvb_mgpu_unique_id(id) and the caller
+ *     broadcasts the FVB_MGPU_ID_BYTES bytes; every rank then calls
+ *     fvb_mgpu_init_rank(nranks, rank, id) with its device current, and
+ *     fvb_mgpu_allreduce_max(rank, buf, stream) per step.
+ * buf is a device pointer to one double; asynchronous on stream.
+ * fvb_mgpu_finalize destroys the communicators. */
+#define FVB_MGPU_ID_BYTES 128
+int fvb_mgpu_unique_id(uint8_t* id_out /* [FVB_MGPU_ID_BYTES] */);
+int fvb_mgpu_init_rank(int nranks, int rank, const uint8_t* id /* [FVB_MGPU_ID_BYTES] */);
+int fvb_mgpu_init(int ndev, const int* devs);
+int fvb_mgpu_allreduce_max(int rank, double* buf, void* stream);
+int fvb_mgpu_allreduce_max_all(double* const* bufs, void* const* streams);
+int fvb_mgpu_finalize(void);
+
 /* FVB1 batch files (host memory, no device work), byte
  * compatible with the reference's fixture dumps save_batch / load_batch
  * (mesh.py:313-353): "FVB1", int64 (d, p, s, N), then QIn, QOut,

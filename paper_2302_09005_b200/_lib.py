@@ -31,7 +31,9 @@ EXPORTED = (
     "fvb_version", "fvb_strerror", "fvb_select_kernel", "fvb_update", "fvb_status_words",
     "fvb_update_host_workspace", "fvb_update_host", "fvb_locate", "fvb_pack", "fvb_unpack",
     "fvb_reduce_dt", "fvb_set_dt", "fvb_patch_max_eig", "fvb_probe", "fvb_selftest_div",
-    "fvb_halo_project", "fvb_halo_project_totals", "fvb_halo_project_window", "fvb_totals_scratch_bytes", "fvb_totals",
+    "fvb_halo_project", "fvb_halo_project_totals", "fvb_halo_project_window",
+    "fvb_mgpu_unique_id", "fvb_mgpu_init_rank", "fvb_mgpu_init", "fvb_mgpu_allreduce_max",
+    "fvb_mgpu_allreduce_max_all", "fvb_mgpu_finalize", "fvb_totals_scratch_bytes", "fvb_totals",
     "fvb_fvb1_header", "fvb_fvb1_read", "fvb_fvb1_write",
 )
 
@@ -93,6 +95,18 @@ def load():
     L.fvb_halo_project_totals.argtypes = [sp, vp, vp, vp, i32, vp, vp, vp]
     L.fvb_halo_project_window.restype = i32
     L.fvb_halo_project_window.argtypes = [sp, vp, vp, vp, vp, vp, i32, i32, vp, vp, vp]
+    L.fvb_mgpu_unique_id.restype = i32
+    L.fvb_mgpu_unique_id.argtypes = [vp]
+    L.fvb_mgpu_init_rank.restype = i32
+    L.fvb_mgpu_init_rank.argtypes = [i32, i32, vp]
+    L.fvb_mgpu_init.restype = i32
+    L.fvb_mgpu_init.argtypes = [i32, vp]
+    L.fvb_mgpu_allreduce_max.restype = i32
+    L.fvb_mgpu_allreduce_max.argtypes = [i32, vp, vp]
+    L.fvb_mgpu_allreduce_max_all.restype = i32
+    L.fvb_mgpu_allreduce_max_all.argtypes = [vp, vp]
+    L.fvb_mgpu_finalize.restype = i32
+    L.fvb_mgpu_finalize.argtypes = []
     L.fvb_totals_scratch_bytes.restype = ctypes.c_size_t
     L.fvb_totals_scratch_bytes.argtypes = [sp]
     L.fvb_totals.restype = i32
