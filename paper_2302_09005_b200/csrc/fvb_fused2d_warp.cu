@@ -93,6 +93,9 @@ __device__ __forceinline__ void sts_q(double* p, const double (&q)[S]) {
   *reinterpret_cast<double2*>(p) = make_double2(q[0], q[1]);
   *reinterpret_cast<double2*>(p + 2) = make_double2(q[2], q[3]);
 }
+#ifndef FVB2D_HALO_LANES
+#define FVB2D_HALO_LANES 1
+#endif
 __device__ __forceinline__ bool inv_ok(double inv) {
   const unsigned e = ((unsigned)__double2hiint(inv) >> 20) & 0x7ffu;
   return inv == 0.0 || (e >= 2u && e < 0x7ffu);
@@ -119,11 +122,18 @@ fused2d_warp_kernel(const double* __restrict__ qin, double* __restrict__ qout, c
   double* outb = wb + W_OUT;
   uint64_t* bars = reinterpret_cast<uint64_t*>(wb + W_BAR);
 
+  // HL (one patch per warp, P + 2 <= 32): lane l owns haloed column l, so the two
+  // x-face halo columns are evaluated by lanes 0 and P+1 in the same pass as the
+  // interior (no separate halo batches) and every lane finds its x neighbours'
+  // data in the same row buffer.
+  constexpr bool HL = PPW == 1 && P + 2 <= 32 && FVB2D_HALO_LANES;
   const int ps = PPW == 2 ? (l & 1) : 0;          // patch slot
-  const int xl = PPW == 2 ? (l >> 1) : l;         // interior column of this lane
-  constexpr bool FULL = PPW == 2 ? P == 16 : P == 32;   // every lane owns a column
-  const bool act = FULL || xl < P;                // lanes past the last column idle
-  const int x = act ? xl : P - 1;                 // (addressing only)
+  const int xl = HL ? l - 1 : (PPW == 2 ? (l >> 1) : l);   // interior column of this lane
+  constexpr bool FULL = !HL && (PPW == 2 ? P == 16 : P == 32);   // every lane owns a column
+  const bool act = FULL || (xl >= 0 && xl < P);   // lanes past the last column idle
+  // (addressing only) HL: lane l addresses haloed column min(l, P+1), i.e. interior column -1 .. P
+  const int x = HL ? (l < E ? l : E - 1) - 1 : (act ? xl : P - 1);
+  const bool hlane = HL && (l == 0 || l == E - 1);        // HL: an x-face halo column
   constexpr int LST = PPW;                        // lane step between x neighbours
   const int64_t items = (n + PPW - 1) / PPW;
   const int64_t gw = (int64_t)blockIdx.x * WPC + warp;
@@ -162,9 +172,9 @@ fused2d_warp_kernel(const double* __restrict__ qin, double* __restrict__ qout, c
 
   // per-lane constant offsets
   const int own = ps * OFFB + (x + 1) * S;          // this lane's volume in a stage
-  const int left = ps * OFFB + x * S;               // x-1 neighbour
-  const int right = ps * OFFB + (x + 2) * S;        // x+1 neighbour
-  const bool lh = x == 0, rh = x == P - 1;          // neighbour is a face-halo column
+  const int left = ps * OFFB + (x < 1 ? 0 : x) * S;              // x-1 neighbour (clamped for halo lanes)
+  const int right = ps * OFFB + (x + 2 > E - 1 ? E - 1 : x + 2) * S;   // x+1 neighbour
+  const bool lh = !HL && x == 0, rh = !HL && x == P - 1;   // neighbour is a face-halo column (halo ring)
   const int lcs = lh ? HXC : 32, rcs = rh ? HXC : 32;   // component strides of the neighbours' x-side data
   (void)lcs;
   (void)rcs;
@@ -218,7 +228,7 @@ fused2d_warp_kernel(const double* __restrict__ qin, double* __restrict__ qout, c
       mbar_wait(&bars[s], par);
 
       // ---- halo columns hx = 0, P+1 of rows hy .. min(hy+3, P) (x-side data only) ----
-      if ((hy & 3) == 1 && hy <= P) {
+      if (!HL && (hy & 3) == 1 && hy <= P) {
 #pragma unroll
         for (int d = 1; d < HB; ++d) {
           const int sd = s + d;
@@ -252,7 +262,8 @@ fused2d_warp_kernel(const double* __restrict__ qin, double* __restrict__ qout, c
         Side<2> sd2[2];
         bool ok;
         closure_all_ranged<2>(q, cl, sd2, ok);
-        slow = slow | !ok;
+        if (HL && hlane) hslow = hslow | !ok;   // x-face halo volume: gated like the reference's face box
+        else slow = slow | !ok;
         const unsigned long long a = (unsigned long long)__double_as_longlong(sd2[0].lam);
         const unsigned long long b = (unsigned long long)__double_as_longlong(sd2[1].lam);
         const unsigned long long m = a > b ? a : b;
@@ -288,8 +299,8 @@ fused2d_warp_kernel(const double* __restrict__ qin, double* __restrict__ qout, c
         // ---- update of this lane's cell of row hy-1 (interior row hy-2) ----
         const double* xr = xsb + ((hy - 1) & 1) * XSD;
         const double* hr = hxs + ((hy - 2) & (HXR - 1)) * 4 + ps;   // halo x-side of row hy-1, side 0
-        const double* ml = lh ? hr : xr + (l - LST);
-        const double* mr = rh ? hr + 2 : xr + (l + LST);
+        const double* ml = lh ? hr : xr + (HL && l == 0 ? 0 : l - LST);
+        const double* mr = rh ? hr + 2 : xr + (HL && l == 31 ? 31 : l + LST);
         double val[S], qn[S];
 #pragma unroll
         for (int u = 0; u < S; ++u) val[u] = oq[u];                        // _pass_copy
