@@ -129,7 +129,7 @@ class SimulationResult:
 
 
 def run_simulation(db: DeviceBatch, grid_shape, steps: int, cfl: float = 0.4, periodic: bool = True,
-                   kernel="auto", dx: float | None = None) -> SimulationResult:
+                   kernel="auto", dx: float | None = None, graph: bool | None = None) -> SimulationResult:
     """Device-resident time loop on one GPU.
 
     db.QOut holds the initial interior field of a logical uniform patch grid
@@ -142,6 +142,14 @@ def run_simulation(db: DeviceBatch, grid_shape, steps: int, cfl: float = 0.4, pe
     the global wave speed, the totals and the non-physical flag of each step
     land in device histories that are copied back once at the end (a
     NonPhysicalStateError then names the first failing step).
+
+    graph=True captures one step (its ~12 kernel launches and copies) in a CUDA
+    graph and replays it: the step writes its history entries through a device
+    step counter, so every replay is the same graph.  Results are bit-identical
+    to the eager loop (graph=False), which is also the fallback when capture is
+    unavailable.  The step is GPU-bound (the host enqueues ahead), so the graph
+    saves ~1 % per step against a ~3 ms capture: the default (None) replays a
+    graph for runs of 64 steps or more.
     """
     import numpy as np
 
@@ -160,14 +168,39 @@ def run_simulation(db: DeviceBatch, grid_shape, steps: int, cfl: float = 0.4, pe
     stepper = CflStepper(db, cfl=cfl, dx=dx, kernel=kernel)
     stepper.prepass()
     gmax_h[0].copy_(stepper.gmax[0])
-    for k in range(steps):
-        dt_h[k].copy_(stepper.dt_scalar[0])   # the dt this step advances by
-        db.status[1:2].zero_()                # redo count of this launch; status[0] accumulates
+    k_t = torch.zeros(1, dtype=torch.int64, device=dev)    # device step counter (graph mode)
+    tot_cur = torch.empty(s, **f64)
+
+    def step_body():
+        dt_h.index_copy_(0, k_t, stepper.dt_scalar)       # the dt this step advances by
+        db.status[1:2].zero_()                            # redo count of this launch; status[0] accumulates
         db.update(kernel=kernel, zero_status=False)
-        flag_h[k].copy_(db.status[0])
-        stepper.reduce_dt()                   # next step's dt from this step's wave speeds
-        db.halo_project_totals(grid_shape, periodic, tot_h[k + 1], scratch)   # one pass over QOut
-        gmax_h[k + 1].copy_(stepper.gmax[0])
+        flag_h.index_copy_(0, k_t, db.status[0:1])
+        stepper.reduce_dt()                               # next step's dt from this step's wave speeds
+        db.halo_project_totals(grid_shape, periodic, tot_cur, scratch)   # one pass over QOut
+        k_t.add_(1)
+        tot_h.index_copy_(0, k_t, tot_cur[None])
+        gmax_h.index_copy_(0, k_t, stepper.gmax)
+
+    g = None
+    if graph is None:
+        graph = steps >= 64
+    if graph and steps > 1:
+        try:
+            side = torch.cuda.Stream(device=dev)
+            side.wait_stream(torch.cuda.current_stream(dev))
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, stream=side, capture_error_mode="thread_local"):
+                step_body()
+        except Exception:   # pragma: no cover - capture unavailable: eager loop
+            g = None
+            torch.cuda.synchronize(dev)
+    if g is not None:
+        for _ in range(steps):
+            g.replay()
+    else:
+        for _ in range(steps):
+            step_body()
 
     flags = flag_h.cpu().numpy()[:steps]
     bad = np.flatnonzero(flags)

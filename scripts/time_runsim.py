@@ -2,6 +2,7 @@
 
     python scripts/time_runsim.py          # moving fluid with a random density perturbation
     python scripts/time_runsim.py --sod    # Sod shock tube along x: fluid at rest (exact +0 momentum)
+    --eager                                # step by step instead of replaying the captured CUDA graph
 """
 import sys
 import time
@@ -27,11 +28,12 @@ else:
     q[...] = state
     q[:, :, 0] += 0.1 * torch.rand(n, p ** 3, device="cuda", dtype=torch.float64)
 db.cell_size.fill_(1.0 / 16)
-driver.run_simulation(db, g, steps=2)
+driver.run_simulation(db, g, steps=2, graph="--eager" not in sys.argv)
 torch.cuda.synchronize()
-for steps in (10, 40):
+graph = "--eager" not in sys.argv
+for steps in (10, 40, 200):
     t0 = time.perf_counter()
-    res = driver.run_simulation(db, g, steps=steps)
+    res = driver.run_simulation(db, g, steps=steps, graph=graph)
     torch.cuda.synchronize()
     dt = time.perf_counter() - t0
     print(f"run_simulation {steps} steps: {dt / steps * 1e3:.3f} ms/step, {n * p**3 * steps / dt / 1e9:.2f} Gcell/s")

@@ -247,3 +247,20 @@ def test_run_simulation_sharded_single_rank_matches(dim, p, grid, periodic):
     assert_bits_equal(sg.db.QOut.cpu().numpy(), db.QOut.cpu().numpy(), "QOut after 6 steps")
     assert res.dt == ref.dt
     np.testing.assert_allclose(np.asarray(res.totals), np.asarray(ref.totals), rtol=1e-13)
+
+
+@pytest.mark.parametrize("dim,p,grid", [(3, 16, (2, 2, 3)), (2, 17, (3, 4)), (3, 4, (3, 3, 3))])
+def test_run_simulation_graph_matches_eager(dim, p, grid):
+    """run_simulation's CUDA-graph step replay gives the eager loop's field and histories bit for bit."""
+    n = int(np.prod(grid))
+    q = oracle.synthetic_qin(dim, p, n, seed=21).reshape(n, (p + 2) ** dim, dim + 2)
+    sl = (slice(None),) + (slice(1, -1),) * dim + (slice(None),)
+    interior = q.reshape((n,) + (p + 2,) * dim + (dim + 2,))[sl].reshape(n, -1)
+    dbs, res = [], []
+    for graph in (False, True):
+        db = _db_with_field(dim, p, grid, interior)
+        res.append(driver.run_simulation(db, grid, steps=7, cfl=0.4, periodic=True, graph=graph))
+        dbs.append(db)
+    assert_bits_equal(dbs[1].QOut.cpu().numpy(), dbs[0].QOut.cpu().numpy(), "QOut")
+    assert res[1].dt == res[0].dt and res[1].max_eigenvalue == res[0].max_eigenvalue
+    assert_bits_equal(np.asarray(res[1].totals), np.asarray(res[0].totals), "totals")
