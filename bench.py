@@ -389,8 +389,9 @@ def main():
                          "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_kind})"},
             "cpu_baseline": cpu,
             "e2e": e2e,
-            # per step: the update kernel (+ the fused path's redo pass) + reduce_max + set_dt
-            "gpu_launches": args.steps * ((2 if kernel_name == "fused" else 1) + 2),
+            # per step: the update kernel (+ the fused path's redo pass) + the dt reduction
+            # (one kernel up to 16,384 patches, else reduce_max_grid + set_dt)
+            "gpu_launches": args.steps * ((2 if kernel_name == "fused" else 1) + (1 if n <= 16384 else 2)),
             "clocks": clocks.summary(),
         }
         print(json.dumps(line), flush=True)
