@@ -54,6 +54,19 @@ def algorithmic_bytes_per_patch(dim: int, p: int) -> int:
     return (p ** dim + 2 * dim * p ** (dim - 1)) * s * 8 + p ** dim * s * 8 + 24
 
 
+def algorithmic_flops_per_cell(dim: int, p: int) -> float:
+    """add/sub/mul/div/sqrt/max = 1 flop (abs = 0) per interior cell update:
+    closures on interior + face-halo volumes, face terms, and the per-cell accumulation."""
+    s = dim + 2
+    vols = p ** dim + 2 * dim * p ** (dim - 1)
+    faces = dim * (p + 1) * p ** (dim - 1)
+    return (vols * (dim * dim + 8 * dim + 7) + faces * (2 + 4 * s)) / p ** dim + 5 * dim * s
+
+
+# B200 FP64: 64 lanes/clk/SM (measured, scripts/micro/lat.cu) x 2 (DFMA) x 148 SMs x 1.965 GHz
+FP64_PEAK_TFLOPS = 64 * 2 * 148 * 1.965e9 / 1e12
+
+
 def measured_peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -310,6 +323,7 @@ def main():
 
     peaks, peak_kind = measured_peaks()
     bytes_per_launch = n * algorithmic_bytes_per_patch(dim, p)
+    flops_cell = algorithmic_flops_per_cell(dim, p)
     achieved = bytes_per_launch / (kern_ms * 1e-3) / 1e9
     traffic = None
     prof = os.path.join(ROOT, "profiles", "ncu_traffic.json")
@@ -387,6 +401,13 @@ def main():
                          "frac": achieved / peaks["hbm_gbs"], "traffic": traffic,
                          "kernel_ms": kern_ms, "algorithmic_bytes_per_launch": bytes_per_launch,
                          "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_kind})"},
+            # the min(HBM, FP64) roofline of the north star: the FP64 side at the algorithmic
+            # flop count (the exact recipe issues ~1.3x more FP64 instructions)
+            "roofline_fp64": {"achieved": flops_cell * cells_per_gpu / (kern_ms * 1e-3) / 1e12,
+                              "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
+                              "frac": flops_cell * cells_per_gpu / (kern_ms * 1e-3) / 1e12 / FP64_PEAK_TFLOPS,
+                              "flops_per_cell": flops_cell,
+                              "cells_per_s_at_peak": FP64_PEAK_TFLOPS * 1e12 / flops_cell},
             "cpu_baseline": cpu,
             "e2e": e2e,
             # per step: the update kernel (+ the fused path's redo pass) + the dt reduction

@@ -26,3 +26,19 @@ def test_reference_arm_nonzero_rank_exits_quietly():
     out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference", "--steps", "1"],
                          capture_output=True, text=True, env=env, timeout=120, check=True)
     assert out.stdout.strip() == ""
+
+
+def test_roofline_definitions_match_survey():
+    """algorithmic bytes per patch and flops per cell for the bench configs."""
+    import importlib.util
+
+    spec = importlib.util.spec_from_file_location("bench", os.path.join(ROOT, "bench.py"))
+    b = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(b)
+    assert b.algorithmic_bytes_per_patch(2, 16) == 18_456
+    assert b.algorithmic_bytes_per_patch(3, 16) == 389_144
+    assert b.algorithmic_bytes_per_patch(3, 4) == 8_984
+    assert abs(b.algorithmic_flops_per_cell(2, 16) - 112.0) < 0.05
+    assert abs(b.algorithmic_flops_per_cell(3, 16) - 200.1) < 0.05
+    assert abs(b.algorithmic_flops_per_cell(3, 4) - 257.5) < 0.05
+    assert abs(b.FP64_PEAK_TFLOPS - 37.2) < 0.1
