@@ -6,7 +6,8 @@
 One step = one fused Rusanov update of the rank's shard (device resident) plus
 the CFL step control: local max wave speed, NCCL MAX all-reduce when N > 1,
 dt = (cfl*dx)/gmax written back on the device (driver.CflStepper).  Weak
-scaling: every rank owns the configuration's full patch count.
+scaling (default): every rank owns the configuration's full patch count;
+--scaling strong splits the configuration's patches over the ranks instead.
 
 Rank 0 prints one JSON line (the driver contract).  `value` is device-timed
 (CUDA events, max over ranks); `e2e` is the drop-in public API
@@ -235,6 +236,7 @@ def main():
     ap.add_argument("--kernel", default="auto", choices=["auto", "fused", "generic"])
     ap.add_argument("--e2e-steps", type=int, default=8)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"])
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
@@ -259,6 +261,10 @@ def main():
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 
     dim, p, n, cfg_idx = CONFIGS[args.config]
+    n_total = n * world   # weak: every rank the configuration's count
+    if args.scaling == "strong":   # the configuration's patches shared by the ranks
+        lo, hi = driver.shard_bounds(n, rank, world)
+        n_total, n = n, hi - lo
     spec = mesh.PatchSpec(dim, p, dim + 2)
     gamma = 1.4
     # synthetic admissible states, generated on the device in slabs
@@ -318,7 +324,8 @@ def main():
     if db.nonphysical():
         raise RuntimeError("non-physical state during the timed steps")
     cells_per_gpu = n * p ** dim
-    value = world * cells_per_gpu * args.steps / (total_ms * 1e-3)
+    total_cells = n_total * p ** dim
+    value = total_cells * args.steps / (total_ms * 1e-3)
     ms_per_step = total_ms / args.steps
 
     peaks, peak_kind = measured_peaks()
@@ -370,7 +377,7 @@ def main():
             e2e_ms = float(t[0])
         h2d_b = int(host.QIn.nbytes + host.cell_size.nbytes + host.dt.nbytes)
         d2h_b = int(host.QOut.nbytes + host.max_eigenvalue.nbytes)
-        e2e = {"value": world * cells_per_gpu * args.e2e_steps / (e2e_ms * 1e-3), "unit": "cell updates/s",
+        e2e = {"value": total_cells * args.e2e_steps / (e2e_ms * 1e-3), "unit": "cell updates/s",
                "h2d_bytes_per_step": h2d_b, "d2h_bytes_per_step": d2h_b,
                "steps": args.e2e_steps, "path": "kernel.update_patch_batch (pinned numpy in, numpy out)"}
         # e2e roofline: the PCIe link, both directions busy at once (copies of chunk k+1 in,
@@ -378,7 +385,7 @@ def main():
         bw = pcie_bandwidth(torch)
         t_bound = max(h2d_b / (bw["h2d"] * 1e9), d2h_b / (bw["d2h"] * 1e9),
                       (h2d_b + d2h_b) / (2.0 * bw["bidir_each"] * 1e9))
-        bound = world * cells_per_gpu / t_bound
+        bound = total_cells / t_bound
         e2e["pcie_gbs"] = {k: round(v, 2) for k, v in bw.items()}
         e2e["roofline"] = {"bound": "pcie", "value": bound, "frac": e2e["value"] / bound}
         del host
@@ -391,9 +398,12 @@ def main():
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": "cell updates/s", "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
+            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": args.scaling,
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": f"{dim}D Euler p={p}, {n} patches per GPU ({_cfg_label(cfg_idx)})",
+            "config": {"workload": (f"{dim}D Euler p={p}, {n} patches per GPU ({_cfg_label(cfg_idx)})"
+                                    if args.scaling == "weak" else
+                                    f"{dim}D Euler p={p}, {n_total} patches over {world} GPU(s) "
+                                    f"({_cfg_label(cfg_idx)}, strong scaling)"),
                        "dim": dim, "p": p, "patches_per_gpu": n, "layout": args.layout, "kernel": kernel_name,
                        "parallelism": f"patch shards x{world}, NCCL MAX all-reduce of the wave speed",
                        "l2": f"inputs {n * spec.haloed_volumes * spec.unknowns * 8 / 1e6:.0f} MB > 126 MB L2; no flush"},
