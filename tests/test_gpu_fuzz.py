@@ -1,0 +1,78 @@
+"""Seeded randomized parity sweep (B200): shapes, layouts, kernels and value sets drawn at
+random -- admissible states with +-0.0 and tiny momenta, huge / tiny scales, zero dt, varied
+cell sizes, occasionally inadmissible volumes -- each checked against the CPU oracle: bit for
+bit when the reference succeeds, and the non-physical flag when it raises."""
+
+import numpy as np
+import pytest
+
+import oracle
+from conftest import assert_bits_equal
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():  # pragma: no cover
+    pytest.skip("no CUDA device", allow_module_level=True)
+
+from paper_2302_09005_b200 import device, mesh  # noqa: E402
+
+SHAPES_2D = list(range(2, 33)) + [40]
+SHAPES_3D = [2, 3, 4, 4, 5, 6, 7, 8, 8, 9, 16, 16, 16, 17]   # fused shapes weighted up
+
+
+def _case(seed):
+    rng = np.random.default_rng(seed)
+    dim = int(rng.choice([2, 3]))
+    p = int(rng.choice(SHAPES_2D if dim == 2 else SHAPES_3D))
+    cells = p ** dim
+    n = int(rng.integers(1, max(2, min(400, 60000 // cells))))
+    layout = "soa" if rng.random() < 0.25 else "aos"
+    kernel = "generic" if rng.random() < 0.15 else "auto"
+    gamma = float(rng.choice([1.4, 5.0 / 3.0]))
+    s = dim + 2
+    v = (p + 2) ** dim
+    scale = 10.0 ** rng.uniform(-30, 30) if rng.random() < 0.2 else 1.0
+    rho = rng.uniform(0.5, 2.0, (n, v)) * scale
+    vel = rng.uniform(-1.0, 1.0, (n, v, dim))
+    pr = rng.uniform(0.5, 2.0, (n, v)) * scale
+    mode = rng.random()
+    if mode < 0.3:                                   # fluid at rest in some components / patches
+        vel[rng.random((n, v, dim)) < 0.4] = 0.0
+    elif mode < 0.4:                                 # signed zeros
+        vel[rng.random((n, v, dim)) < 0.3] = -0.0
+    elif mode < 0.5:                                 # tiny momenta (outside the fast range)
+        vel[rng.random((n, v, dim)) < 0.05] = 1e-70
+    q = np.empty((n, v, s))
+    q[..., 0] = rho
+    q[..., 1:1 + dim] = rho[..., None] * vel
+    q[..., -1] = pr / (gamma - 1.0) + 0.5 * rho * np.sum(vel * vel, axis=-1)
+    if rng.random() < 0.1:                           # an inadmissible volume somewhere
+        k = rng.integers(n)
+        q[k, rng.integers(v), -1] = -1.0 * scale
+    cs = rng.uniform(0.25, 4.0, n)
+    c_max = np.sqrt(gamma * 4.0) + 1.0
+    dt = rng.uniform(0.0, 0.4, n) * (cs / p) / c_max
+    dt[rng.random(n) < 0.1] = 0.0
+    return dim, p, n, layout, kernel, gamma, q.reshape(n, -1), cs, dt
+
+
+@pytest.mark.parametrize("seed", range(128))
+def test_fuzz_vs_oracle(seed):
+    dim, p, n, layout, kernel, gamma, qin, cs, dt = _case(seed)
+    if kernel == "auto" and layout == "soa" and device.selected_kernel(dim, p, n, gamma, "soa") != "fused":
+        kernel = "auto"
+    spec = mesh.PatchSpec(dim, p, dim + 2)
+    b = mesh.make_patch_batch(spec, n)
+    b.QIn[...] = qin
+    b.cell_size[...] = cs[:, None]
+    b.dt[...] = dt
+    ref_q, ref_l, st = oracle.update(dim, p, gamma, b.QIn, b.cell_size, b.dt)
+    db = device.DeviceBatch.from_host(b, gamma, layout=layout)
+    db.update(kernel=kernel)
+    out = mesh.make_patch_batch(spec, n)
+    db.to_host(out)
+    what = f"seed {seed}: {dim}D p={p} n={n} {layout} {kernel} gamma={gamma:.3f}"
+    assert db.nonphysical() == (st != 0), what
+    if st == 0:
+        assert_bits_equal(out.QOut, ref_q, what)
+        assert_bits_equal(out.max_eigenvalue, ref_l, what + " max_eig")
