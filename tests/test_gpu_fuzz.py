@@ -76,3 +76,44 @@ def test_fuzz_vs_oracle(seed):
     if st == 0:
         assert_bits_equal(out.QOut, ref_q, what)
         assert_bits_equal(out.max_eigenvalue, ref_l, what + " max_eig")
+
+
+@pytest.mark.parametrize("seed", range(32))
+def test_fuzz_drop_in_vs_oracle(seed):
+    """The drop-in update_patch_batch on host arrays (chunked H2D / kernel / D2H pipeline with a
+    random chunk size, random variant labels): bits when admissible; when not, the same
+    NonPhysicalStateError patch and volume the reference's engine would raise first."""
+    from paper_2302_09005_b200 import kernel as K
+    from paper_2302_09005_b200 import pde
+    from paper_2302_09005_b200.errors import NonPhysicalStateError
+
+    dim, p, n, _, _, gamma, qin, cs, dt = _case(1000 + seed)
+    rng = np.random.default_rng(seed)
+    if rng.random() < 0.35:   # make some batches inadmissible on purpose
+        q = qin.reshape(n, -1, dim + 2)
+        k = rng.integers(n, size=int(rng.integers(1, 4)))
+        q[k, rng.integers(q.shape[1], size=k.size), 0] = -1.0
+    ordering = str(rng.choice(["patchwise", "batched"]))
+    strategy = str(rng.choice(["seq", "par"]))
+    variant = K.variant_from_labels(ordering, "aos", strategy, int(rng.integers(1, 9)))
+    chunk = None if rng.random() < 0.5 else int(rng.integers(1, n + 1))
+    spec = mesh.PatchSpec(dim, p, dim + 2)
+    b = mesh.make_patch_batch(spec, n)
+    b.QIn[...] = qin
+    b.cell_size[...] = cs[:, None]
+    b.dt[...] = dt
+    euler = pde.make_euler_pde(dim, pde.EulerParameters(gamma))
+    ref_q, ref_l, st = oracle.update(dim, p, gamma, b.QIn, b.cell_size, b.dt)
+    what = f"seed {seed}: {dim}D p={p} n={n} {ordering}/{strategy} chunk={chunk}"
+    if st == 0:
+        K.update_patch_batch(b, euler, variant, chunk_patches=chunk)
+        assert_bits_equal(b.QOut, ref_q, what)
+        assert_bits_equal(b.max_eigenvalue, ref_l, what + " max_eig")
+        return
+    info = oracle.locate(dim, p, gamma, b.QIn)
+    nch = K.host_chunks(variant, n) if ordering == "batched" else 1
+    patch, box, lin, _ = oracle.first_error(dim, p, info, 0 if ordering == "patchwise" else 1, nch)
+    with pytest.raises(NonPhysicalStateError) as ei:
+        K.update_patch_batch(b, euler, variant, chunk_patches=chunk)
+    assert ei.value.patch == patch, what
+    assert tuple(ei.value.volume) == tuple(oracle.box_volume(dim, p, box, lin)), what
