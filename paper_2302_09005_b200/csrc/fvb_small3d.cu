@@ -103,7 +103,7 @@ constexpr bool TOUT = FVB_SMALL3D_TOUT != 0;
 // skipped): p = 8 1,047 -> 1,034 us; p = 4 2.74 -> 2.84 ms (the extra TMA ops
 // cost more than the 8 % of bytes), so only for p >= 6.
 #ifndef FVB_SMALL3D_TRIM
-#define FVB_SMALL3D_TRIM (P >= 6)
+#define FVB_SMALL3D_TRIM (P >= 6 && !(P & 1))
 #endif
 #ifndef FVB_SMALL3D_REMAP
 #define FVB_SMALL3D_REMAP 1
@@ -116,6 +116,12 @@ small3d_kernel(const double* __restrict__ qin, double* __restrict__ qout, const 
                int64_t n_patches, Closure cl, const __grid_constant__ CUtensorMap omap) {
   using C = Cfg<P>;
   constexpr int S = C::S, E = C::E;
+  // Odd P: a patch is an odd multiple of 8 bytes, so neither the bulk copies nor the
+  // tensor store (16-byte granularity) can address it.  The CTA stages it with 8-byte
+  // cp.async copies into the same ring (the mbarrier counts every thread's arrive),
+  // and writes the output back with coalesced 8-byte stores.
+  constexpr bool ODD = (P & 1) != 0;
+  constexpr bool TOUT_P = TOUT && !ODD;
   extern __shared__ __align__(128) double sm[];
   double* ring = sm + C::OFF_RING;
   double* sideb = sm + C::OFF_SIDE;
@@ -167,14 +173,26 @@ small3d_kernel(const double* __restrict__ qin, double* __restrict__ qout, const 
     }
   };
 
+  auto issue_coop = [&](int g) {   // odd P: every thread copies its share, then arrives
+    const int64_t grp = group_of(g);
+    const int np = patches_in(grp);
+    double* st = ring + (g % C::NST) * C::STAGE;
+    const double* src = qin + grp * C::PPC * (int64_t)C::VOL * S;
+    for (int i = tid; i < np * C::VOL * S; i += C::THREADS) cp_async8(st + i, src + i);
+    cp_async_mbar_arrive_noinc(bars + (g % C::NST));
+  };
+
   if (tid == 0) {
-    for (int s = 0; s < C::NST; ++s) mbar_init(&bars[s], 1);
+    for (int s = 0; s < C::NST; ++s) mbar_init(&bars[s], ODD ? C::THREADS : 1);
     slowflag[0] = slowflag[1] = 0;
     fence_mbar_init();
   }
   __syncthreads();
-  if (tid == 0)
+  if (ODD) {
+    for (int g = 0; g < C::NST && g < G; ++g) issue_coop(g);
+  } else if (tid == 0) {
     for (int g = 0; g < C::NST && g < G; ++g) issue(g);
+  }
 
   unsigned stg = 0, par = 0;
   // per-patch scalars, loaded one iteration ahead (their latency used to stall the closures)
@@ -334,11 +352,11 @@ small3d_kernel(const double* __restrict__ qin, double* __restrict__ qout, const 
           val[u] = dadd(val[u], dmul(half_inv, dsub(dadd(fm, fc), dadd(fc, fp))));
         }
       }
-      const int lin = TOUT ? (cy * P + cz) * P + cx    // staging order (x, z, y), see TOUT
-                           : (cz * P + cy) * P + cx;   // AoS interior order (x fastest)
+      const int lin = TOUT_P ? (cy * P + cz) * P + cx    // staging order (x, z, y), see TOUT
+                             : (cz * P + cy) * P + cx;   // AoS interior order (x fastest)
 #pragma unroll
       for (int u = 0; u < S; ++u) outb[(g % C::NOB) * C::OUTN + (lp * C::IVOL + lin) * S + u] = val[u];
-      fence_proxy_async();
+      if (!ODD) fence_proxy_async();
     }
     // per-patch max wave speed: 64-bit max as (high word, low word) warp reductions
     {
@@ -351,12 +369,12 @@ small3d_kernel(const double* __restrict__ qin, double* __restrict__ qout, const 
     __syncthreads();
     if (tid == 0) {
       // output of this group, per-patch maxima, redo list; then refill the freed stage
-      if (TOUT)
+      if (TOUT_P)
         tma_store_4d(&omap, 0, 0, 0, (int)(grp * C::PPC), outb + (g % C::NOB) * C::OUTN);
-      else
+      else if (!ODD)
         tma_store_1d(qout + grp * C::PPC * (int64_t)C::IVOL * S, outb + (g % C::NOB) * C::OUTN,
                      (uint32_t)(np * C::IVOL * S * 8));
-      bulk_commit();
+      if (!ODD) bulk_commit();
       const unsigned flags = slowflag[g & 1];
       for (int k = 0; k < np; ++k) {
         unsigned long long m = 0;
@@ -371,7 +389,13 @@ small3d_kernel(const double* __restrict__ qin, double* __restrict__ qout, const 
         }
       }
       slowflag[g & 1] = 0;   // next set in iteration g+2, after the next barrier
-      if (g + C::NST < G) issue(g + C::NST);   // stage of this group, fully consumed
+      if (!ODD && g + C::NST < G) issue(g + C::NST);   // stage of this group, fully consumed
+    }
+    if (ODD) {   // coalesced write-back of the staged output, then refill the consumed stage
+      const double* ob = outb + (g % C::NOB) * C::OUTN;
+      double* dst = qout + grp * C::PPC * (int64_t)C::IVOL * S;
+      for (int i = tid; i < np * C::IVOL * S; i += C::THREADS) dst[i] = ob[i];
+      if (g + C::NST < G) issue_coop(g + C::NST);
     }
     stg = stg == C::NST - 1 ? 0 : stg + 1;
     par ^= (stg == 0);
@@ -397,7 +421,7 @@ cudaError_t launch(const FvbArgs& a, cudaStream_t st) {
   const Closure cl{a.gamma, a.gamma - 1.0};
   CUtensorMap omap;
   memset(&omap, 0, sizeof(omap));
-  if (TOUT) {   // QOut as {x*S, z, y, patch}: the staging's (x, z, y) order, AoS in memory
+  if (TOUT && !(P & 1)) {   // QOut as {x*S, z, y, patch}: the staging's (x, z, y) order, AoS in memory
     EncodeTiledFn enc = encode_tiled();
     if (!enc) return cudaErrorNotSupported;
     const cuuint64_t dims[4] = {(cuuint64_t)P * C::S, (cuuint64_t)P, (cuuint64_t)P, (cuuint64_t)a.n};
@@ -418,11 +442,13 @@ cudaError_t launch(const FvbArgs& a, cudaStream_t st) {
 }  // namespace fs
 }  // namespace fvb
 
-// 3D AoS patches of even p = 2 .. 8 (one patch per CTA; p = 4 has the tuned halo split).
-// Odd p would make the haloed / interior patch sizes odd multiples of 8 bytes,
-// which the TMA bulk copies (16-byte granularity) cannot address per patch.
+// 3D AoS patches of p = 2, 4 .. 8 (one patch per CTA; p = 4 has the tuned halo split).
+// Odd p makes the haloed / interior patch sizes odd multiples of 8 bytes, which the
+// TMA bulk copies (16-byte granularity) cannot address per patch: those stage with
+// 8-byte cp.async copies and write back with plain stores (ODD in the kernel).
 bool fvb_small3d_supported(int dim, int p, int layout) {
-  return dim == 3 && p >= 2 && p <= 8 && (p & 1) == 0 && layout == fvb::kAoS;
+  // p = 3 stays on the generic kernel: 27 cells fill one warp poorly (measured 9.2 vs 9.8 Gcell/s)
+  return dim == 3 && p >= 2 && p <= 8 && p != 3 && layout == fvb::kAoS;
 }
 
 cudaError_t fvb_launch_small3d(const FvbArgs& a, cudaStream_t st) {
@@ -431,6 +457,8 @@ cudaError_t fvb_launch_small3d(const FvbArgs& a, cudaStream_t st) {
   switch (a.p) {
     case 2: e = fvb::fs::launch<2>(a, st); break;
     case 4: e = fvb::fs::launch<4>(a, st); break;
+    case 5: e = fvb::fs::launch<5>(a, st); break;
+    case 7: e = fvb::fs::launch<7>(a, st); break;
     case 6: e = fvb::fs::launch<6>(a, st); break;
     case 8: e = fvb::fs::launch<8>(a, st); break;
     default: return cudaErrorInvalidValue;

@@ -46,8 +46,9 @@ def test_capi_contract_checks_without_gpu():
     assert L.fvb_select_kernel(ctypes.byref(_lib.spec(3, 16, 5, 1.4))) == _lib.KERNEL_FUSED
     assert L.fvb_select_kernel(ctypes.byref(_lib.spec(3, 4, 5, 1.4))) == _lib.KERNEL_FUSED
     assert L.fvb_select_kernel(ctypes.byref(_lib.spec(3, 4, 5, 1.4, 1))) == _lib.KERNEL_GENERIC
-    assert L.fvb_select_kernel(ctypes.byref(_lib.spec(3, 6, 5, 1.4))) == _lib.KERNEL_FUSED     # even p = 2..8
-    assert L.fvb_select_kernel(ctypes.byref(_lib.spec(3, 5, 5, 1.4))) == _lib.KERNEL_GENERIC
+    assert L.fvb_select_kernel(ctypes.byref(_lib.spec(3, 6, 5, 1.4))) == _lib.KERNEL_FUSED     # p = 2..8
+    assert L.fvb_select_kernel(ctypes.byref(_lib.spec(3, 5, 5, 1.4))) == _lib.KERNEL_FUSED     # odd p: cp.async
+    assert L.fvb_select_kernel(ctypes.byref(_lib.spec(3, 3, 5, 1.4))) == _lib.KERNEL_GENERIC   # p = 3: generic
     assert L.fvb_select_kernel(ctypes.byref(_lib.spec(3, 9, 5, 1.4))) == _lib.KERNEL_GENERIC
     assert L.fvb_select_kernel(ctypes.byref(_lib.spec(3, 6, 5, 1.4, 1))) == _lib.KERNEL_GENERIC   # SoA
     assert L.fvb_select_kernel(ctypes.byref(_lib.spec(2, 16, 5, 1.4, 1))) == _lib.KERNEL_FUSED
