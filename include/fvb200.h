@@ -170,6 +170,14 @@ int fvb_halo_project_window(const fvb_spec* spec, const double* ghost_lo, const 
                             const double* ghost_hi, double* qin, const int32_t* window_grid, int32_t lo_layers,
                             int periodic_mask, double* scratch, double* totals, void* stream);
 
+/* Page-lock a caller's host range for the H2D / D2H of fvb_update_host (pageable
+ * copies are driver-staged and synchronous: ~6.7x slower for C3).  Returns FVB_OK when
+ * registered, 1 when the range is already page-locked (nothing to undo), FVB_ERR_CUDA
+ * when it cannot be (the call then still works on pageable memory).  fvb_host_unpin
+ * releases a range fvb_host_pin registered. */
+int fvb_host_pin(const void* p, size_t bytes);
+int fvb_host_unpin(const void* p);
+
 /* Multi-GPU: the step's single exchange, a MAX all-reduce of the global wave
  * speed (one fp64) over NCCL on NVLink / NVSwitch (the
  * ncclAllReduce of the north star), for hosts that do not use torch.distributed.

@@ -219,6 +219,28 @@ int fvb_update_host(const fvb_spec* spec, const double* qin_h, double* qout_h, c
   return (st_h[0] | st_h[1]) ? FVB_ERR_NONPHYSICAL : FVB_OK;
 }
 
+int fvb_host_pin(const void* p, size_t bytes) {
+  if (!p || bytes == 0) return set_contract("null host range");
+  cudaPointerAttributes at;
+  if (cudaPointerGetAttributes(&at, p) == cudaSuccess && at.type == cudaMemoryTypeHost) return 1;   // already
+  cudaGetLastError();
+  const cudaError_t e = cudaHostRegister(const_cast<void*>(p), bytes, cudaHostRegisterDefault);
+  if (e != cudaSuccess) {
+    cudaGetLastError();   // leave no stale error for the next launch check
+    return set_cuda_error(e, "cudaHostRegister");
+  }
+  return FVB_OK;
+}
+
+int fvb_host_unpin(const void* p) {
+  const cudaError_t e = cudaHostUnregister(const_cast<void*>(p));
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return set_cuda_error(e, "cudaHostUnregister");
+  }
+  return FVB_OK;
+}
+
 int fvb_locate(const fvb_spec* spec, const double* qin, fvb_boxinfo* info, void* stream) {
   int rc = check_spec(spec);
   if (rc) return rc;
