@@ -156,21 +156,41 @@ int fvb_update_host(const fvb_spec* spec, const double* qin_h, double* qout_h, c
     me_d[b] = reinterpret_cast<double*>(p);
   }
   cudaStream_t comp = as_stream(stream);
-  cudaStream_t h2d = nullptr, d2h = nullptr;
-  cudaEvent_t ev_in[2] = {nullptr, nullptr}, ev_k[2] = {nullptr, nullptr}, ev_out[2] = {nullptr, nullptr};
-  cudaError_t e = cudaStreamCreateWithFlags(&h2d, cudaStreamNonBlocking);
-  if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&d2h, cudaStreamNonBlocking);
-  for (int b = 0; b < 2 && e == cudaSuccess; ++b) {
-    e = cudaEventCreateWithFlags(&ev_in[b], cudaEventDisableTiming);
-    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ev_k[b], cudaEventDisableTiming);
-    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ev_out[b], cudaEventDisableTiming);
+  // copy streams and events: created once per thread and device, reused by every call
+  // (creating them per call cost ~0.1 ms, most of a small batch's latency)
+  struct Pipe {
+    int dev = -1;
+    cudaStream_t h2d = nullptr, d2h = nullptr;
+    cudaEvent_t ev_in[2] = {nullptr, nullptr}, ev_k[2] = {nullptr, nullptr}, ev_out[2] = {nullptr, nullptr};
+    cudaEvent_t ev_start = nullptr;
+  };
+  static thread_local Pipe pipes[8];
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return set_cuda_error(e, "cudaGetDevice");
+  Pipe& pp = pipes[dev & 7];
+  if (pp.dev != dev) {
+    pp = Pipe();
+    e = cudaStreamCreateWithFlags(&pp.h2d, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&pp.d2h, cudaStreamNonBlocking);
+    for (int b = 0; b < 2 && e == cudaSuccess; ++b) {
+      e = cudaEventCreateWithFlags(&pp.ev_in[b], cudaEventDisableTiming);
+      if (e == cudaSuccess) e = cudaEventCreateWithFlags(&pp.ev_k[b], cudaEventDisableTiming);
+      if (e == cudaSuccess) e = cudaEventCreateWithFlags(&pp.ev_out[b], cudaEventDisableTiming);
+    }
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&pp.ev_start, cudaEventDisableTiming);
+    if (e != cudaSuccess) return set_cuda_error(e, "fvb_update_host streams");
+    pp.dev = dev;
   }
+  cudaStream_t h2d = pp.h2d, d2h = pp.d2h;
+  cudaEvent_t* ev_in = pp.ev_in;
+  cudaEvent_t* ev_k = pp.ev_k;
+  cudaEvent_t* ev_out = pp.ev_out;
   // flag words of both status buffers accumulate over the chunks; redo counts are reset per chunk
   if (e == cudaSuccess) e = cudaMemsetAsync(status_b[0], 0, 8, comp);
   if (e == cudaSuccess) e = cudaMemsetAsync(status_b[1], 0, 8, comp);
   // the copy streams must not run ahead of the status reset / earlier work on `comp`
-  cudaEvent_t ev_start = nullptr;
-  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ev_start, cudaEventDisableTiming);
+  cudaEvent_t ev_start = pp.ev_start;
   if (e == cudaSuccess) e = cudaEventRecord(ev_start, comp);
   if (e == cudaSuccess) e = cudaStreamWaitEvent(h2d, ev_start, 0);
   int nch = (int)((n + chunk - 1) / chunk);
@@ -206,15 +226,11 @@ int fvb_update_host(const fvb_spec* spec, const double* qin_h, double* qout_h, c
   if (e == cudaSuccess) e = cudaStreamSynchronize(comp);
   if (e == cudaSuccess) e = cudaMemcpy(&st_h[0], status_b[0], sizeof(uint32_t), cudaMemcpyDeviceToHost);
   if (e == cudaSuccess) e = cudaMemcpy(&st_h[1], status_b[1], sizeof(uint32_t), cudaMemcpyDeviceToHost);
-  for (int b = 0; b < 2; ++b) {
-    if (ev_in[b]) cudaEventDestroy(ev_in[b]);
-    if (ev_k[b]) cudaEventDestroy(ev_k[b]);
-    if (ev_out[b]) cudaEventDestroy(ev_out[b]);
+  if (krc != FVB_OK) {   // an aborted pipeline may leave copies queued: drain before the buffers are reused
+    cudaStreamSynchronize(h2d);
+    cudaStreamSynchronize(d2h);
+    return krc;
   }
-  if (ev_start) cudaEventDestroy(ev_start);
-  if (h2d) cudaStreamDestroy(h2d);
-  if (d2h) cudaStreamDestroy(d2h);
-  if (krc != FVB_OK) return krc;
   if (e != cudaSuccess) return set_cuda_error(e, "fvb_update_host");
   return (st_h[0] | st_h[1]) ? FVB_ERR_NONPHYSICAL : FVB_OK;
 }

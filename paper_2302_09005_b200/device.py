@@ -258,7 +258,8 @@ def default_chunk(spec: PatchSpec, n: int, pipeline_chunks: int | None = None) -
     by_bytes = max(1, (256 << 20) // per_patch)
     k = int(pipeline_chunks or os.environ.get("FVB_HOST_CHUNKS", "32"))
     by_pipeline = max(1, -(-n // k))
-    return int(max(1, min(n, by_bytes, max(by_pipeline, min(n, 16)))))
+    floor = max(16, -(-(4 << 20) // per_patch))   # >= 4 MB per chunk: small batches are not worth pipelining
+    return int(max(1, min(n, by_bytes, max(by_pipeline, min(n, floor)))))
 
 
 # Page-locking of caller arrays (drop-in path).  Pageable host arrays make every H2D / D2H a
