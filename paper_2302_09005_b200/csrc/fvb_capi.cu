@@ -163,6 +163,7 @@ int fvb_update_host(const fvb_spec* spec, const double* qin_h, double* qout_h, c
     cudaStream_t h2d = nullptr, d2h = nullptr;
     cudaEvent_t ev_in[2] = {nullptr, nullptr}, ev_k[2] = {nullptr, nullptr}, ev_out[2] = {nullptr, nullptr};
     cudaEvent_t ev_start = nullptr;
+    uint32_t* flags = nullptr;   // pinned readback of the two status flags
   };
   static thread_local Pipe pipes[8];
   int dev = 0;
@@ -221,11 +222,19 @@ int fvb_update_host(const fvb_spec* spec, const double* qin_h, double* qout_h, c
     if (e == cudaSuccess) e = cudaMemcpyAsync(max_eig_h + p0, me_d[b], (size_t)np * 8, cudaMemcpyDeviceToHost, d2h);
     if (e == cudaSuccess) e = cudaEventRecord(ev_out[b], d2h);
   }
-  uint32_t st_h[2] = {0, 0};
+  // the two flag words come back with the last D2H (pinned, per thread) instead of two
+  // synchronous copies after the drain
+  if (!pp.flags && e == cudaSuccess) e = cudaMallocHost(reinterpret_cast<void**>(&pp.flags), 2 * sizeof(uint32_t));
+  if (e == cudaSuccess) e = cudaStreamWaitEvent(d2h, ev_k[(nch - 1) & 1], 0);   // every kernel done (comp order)
+  if (e == cudaSuccess) e = cudaMemcpyAsync(&pp.flags[0], status_b[0], 4, cudaMemcpyDeviceToHost, d2h);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(&pp.flags[1], status_b[1], 4, cudaMemcpyDeviceToHost, d2h);
   if (e == cudaSuccess) e = cudaStreamSynchronize(d2h);
   if (e == cudaSuccess) e = cudaStreamSynchronize(comp);
-  if (e == cudaSuccess) e = cudaMemcpy(&st_h[0], status_b[0], sizeof(uint32_t), cudaMemcpyDeviceToHost);
-  if (e == cudaSuccess) e = cudaMemcpy(&st_h[1], status_b[1], sizeof(uint32_t), cudaMemcpyDeviceToHost);
+  uint32_t st_h[2] = {0, 0};
+  if (e == cudaSuccess) {
+    st_h[0] = pp.flags[0];
+    st_h[1] = pp.flags[1];
+  }
   if (krc != FVB_OK) {   // an aborted pipeline may leave copies queued: drain before the buffers are reused
     cudaStreamSynchronize(h2d);
     cudaStreamSynchronize(d2h);
