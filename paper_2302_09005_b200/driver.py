@@ -258,6 +258,29 @@ def exchange_ghost_layers(own, layer_elems: int, ghost_lo, ghost_hi, rank: int, 
         w.wait()
 
 
+def shard_layout(grid_shape, rank: int, world: int, periodic: bool) -> dict:
+    """Host-side geometry of one rank's shard (no device work): its layers [l0, l1) along
+    the slowest axis, its patch range, whether it has a lower / upper ghost layer, the
+    window grid the windowed halo projection sees and the per-axis wrap mask."""
+    from .errors import ContractViolationError
+
+    grid = tuple(int(g) for g in grid_shape)
+    if grid[-1] < world:
+        raise ContractViolationError(f"{world} ranks need at least {world} layers along the sharded "
+                                     f"axis, grid {grid} has {grid[-1]}")
+    layer = 1
+    for g in grid[:-1]:
+        layer *= g
+    l0, l1 = shard_bounds(grid[-1], rank, world)
+    lo, hi = _neighbours(rank, world, periodic)
+    lo_layers, hi_layers = (1 if lo is not None else 0), (1 if hi is not None else 0)
+    return {"layer": layer, "l0": l0, "l1": l1, "patch_lo": l0 * layer, "patch_hi": l1 * layer,
+            "lower": lo, "upper": hi, "lo_layers": lo_layers,
+            "window_grid": grid[:-1] + (lo_layers + (l1 - l0) + hi_layers,),
+            # wrap along x / y (3D) or x (2D); the sharded axis wraps through the ghost layers
+            "pmask": ((1 << (len(grid) - 1)) - 1) if periodic else 0}
+
+
 class ShardedGrid:
     """One rank's shard of a logical uniform patch grid, split in whole layers along the
     slowest axis (z in 3D, y in 2D; patch index x-fastest as in halo_project).
@@ -280,28 +303,17 @@ class ShardedGrid:
         self.rank = rank if rank is not None else (dist.get_rank(group) if on else 0)
         self.world = world if world is not None else (dist.get_world_size(group) if on else 1)
         self.group, self.periodic = group, bool(periodic)
-        layer = 1
-        for g in self.grid[:-1]:
-            layer *= g
-        self.layer = layer
-        if self.grid[-1] < self.world:
-            from .errors import ContractViolationError
-            raise ContractViolationError(f"{self.world} ranks need at least {self.world} layers along the sharded "
-                                         f"axis, grid {self.grid} has {self.grid[-1]}")
-        self.l0, self.l1 = shard_bounds(self.grid[-1], self.rank, self.world)
-        self.patch_lo, self.patch_hi = self.l0 * layer, self.l1 * layer
-        n_own = self.patch_hi - self.patch_lo
-        self.db = DeviceBatch(spec, n_own, gamma, device)
-        self.layer_elems = layer * spec.interior_volumes * spec.unknowns
-        lo, hi = _neighbours(self.rank, self.world, self.periodic)
+        lay = shard_layout(self.grid, self.rank, self.world, self.periodic)
+        self.layer, self.l0, self.l1 = lay["layer"], lay["l0"], lay["l1"]
+        self.patch_lo, self.patch_hi = lay["patch_lo"], lay["patch_hi"]
+        self.db = DeviceBatch(spec, self.patch_hi - self.patch_lo, gamma, device)
+        self.layer_elems = self.layer * spec.interior_volumes * spec.unknowns
         f64 = dict(dtype=torch.float64, device=self.db.device)
-        self.ghost_lo = torch.empty(self.layer_elems, **f64) if lo is not None else None
-        self.ghost_hi = torch.empty(self.layer_elems, **f64) if hi is not None else None
-        self.lo_layers = 1 if lo is not None else 0
-        own_layers = self.l1 - self.l0
-        self.window_grid = self.grid[:-1] + (self.lo_layers + own_layers + (1 if hi is not None else 0),)
-        # wrap along x / y (3D) or x (2D); the sharded axis wraps through the ghost layers
-        self.pmask = ((1 << (d - 1)) - 1) if self.periodic else 0
+        self.ghost_lo = torch.empty(self.layer_elems, **f64) if lay["lower"] is not None else None
+        self.ghost_hi = torch.empty(self.layer_elems, **f64) if lay["upper"] is not None else None
+        self.lo_layers = lay["lo_layers"]
+        self.window_grid = lay["window_grid"]
+        self.pmask = lay["pmask"]
 
     def exchange(self) -> None:
         exchange_ghost_layers(self.db.QOut, self.layer_elems, self.ghost_lo, self.ghost_hi, self.rank, self.world,

@@ -187,3 +187,34 @@ def test_shard_bounds_cover_in_order():
             assert spans[0][0] == 0 and spans[-1][1] == n
             assert all(a[1] == b[0] for a, b in zip(spans, spans[1:]))
             assert max(h - l for l, h in spans) - min(h - l for l, h in spans) <= 1
+
+
+def test_shard_layout_covers_grid_with_ghosts():
+    """driver.shard_layout: shards tile the grid in order; ghost layers exist exactly where a
+    neighbour is (all sides when periodic, none at a non-periodic edge); the window grid is
+    own layers plus ghosts; the wrap mask leaves the sharded axis to the ghosts."""
+    import pytest
+
+    from paper_2302_09005_b200 import driver
+    from paper_2302_09005_b200.errors import ContractViolationError
+
+    for grid in ((4, 3, 7), (5, 9)):
+        for world in (1, 2, 3, 7):
+            for periodic in (True, False):
+                if grid[-1] < world:
+                    with pytest.raises(ContractViolationError):
+                        driver.shard_layout(grid, 0, world, periodic)
+                    continue
+                prev = 0
+                for r in range(world):
+                    lay = driver.shard_layout(grid, r, world, periodic)
+                    assert lay["l0"] == prev and lay["l1"] > lay["l0"]
+                    prev = lay["l1"]
+                    has_lo = periodic or r > 0
+                    has_hi = periodic or r < world - 1
+                    assert (lay["lower"] is not None) == has_lo and (lay["upper"] is not None) == has_hi
+                    assert lay["window_grid"][:-1] == grid[:-1]
+                    assert lay["window_grid"][-1] == (lay["l1"] - lay["l0"]) + has_lo + has_hi
+                    assert lay["pmask"] == (((1 << (len(grid) - 1)) - 1) if periodic else 0)
+                    assert lay["patch_hi"] - lay["patch_lo"] == (lay["l1"] - lay["l0"]) * lay["layer"]
+                assert prev == grid[-1]
