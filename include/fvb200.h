@@ -170,6 +170,17 @@ int fvb_halo_project_window(const fvb_spec* spec, const double* ghost_lo, const 
                             const double* ghost_hi, double* qin, const int32_t* window_grid, int32_t lo_layers,
                             int periodic_mask, double* scratch, double* totals, void* stream);
 
+/* 2D multi-step fast path (run_simulation): the update writes the new state straight
+ * into the interior of the next step's haloed batch qin_next (the warp kernel's TMA
+ * store addresses a haloed row at a 32-byte offset), fvb_halo_shell then fills only
+ * that batch's halo shell from the neighbours' interiors (21 % of the bytes of a full
+ * halo projection), and fvb_totals_haloed sums the interiors for the step's totals.
+ * Bit-identical to fvb_update + fvb_halo_project.  2D AoS, 2 <= p <= 32. */
+int fvb_update_to_haloed(const fvb_spec* spec, const double* qin, double* qin_next, const double* cell_size,
+                         const double* dt, double* max_eig, uint32_t* status, int zero_status, void* stream);
+int fvb_halo_shell(const fvb_spec* spec, double* qin, const int32_t* grid_shape, int periodic, void* stream);
+int fvb_totals_haloed(const fvb_spec* spec, const double* qin, double* scratch, double* totals, void* stream);
+
 /* Page-lock a caller's host range for the H2D / D2H of fvb_update_host (pageable
  * copies are driver-staged and synchronous: ~6.7x slower for C3).  Returns FVB_OK when
  * registered, 1 when the range is already page-locked (nothing to undo), FVB_ERR_CUDA

@@ -32,7 +32,7 @@ EXPORTED = (
     "fvb_update_host_workspace", "fvb_update_host", "fvb_locate", "fvb_pack", "fvb_unpack",
     "fvb_reduce_dt", "fvb_set_dt", "fvb_patch_max_eig", "fvb_probe", "fvb_selftest_div",
     "fvb_halo_project", "fvb_halo_project_totals", "fvb_halo_project_window",
-    "fvb_host_pin", "fvb_host_unpin",
+    "fvb_host_pin", "fvb_host_unpin", "fvb_update_to_haloed", "fvb_halo_shell", "fvb_totals_haloed",
     "fvb_mgpu_unique_id", "fvb_mgpu_init_rank", "fvb_mgpu_init", "fvb_mgpu_allreduce_max",
     "fvb_mgpu_allreduce_max_all", "fvb_mgpu_finalize", "fvb_totals_scratch_bytes", "fvb_totals",
     "fvb_fvb1_header", "fvb_fvb1_read", "fvb_fvb1_write",
@@ -96,6 +96,12 @@ def load():
     L.fvb_halo_project_totals.argtypes = [sp, vp, vp, vp, i32, vp, vp, vp]
     L.fvb_halo_project_window.restype = i32
     L.fvb_halo_project_window.argtypes = [sp, vp, vp, vp, vp, vp, i32, i32, vp, vp, vp]
+    L.fvb_update_to_haloed.restype = i32
+    L.fvb_update_to_haloed.argtypes = [sp, vp, vp, vp, vp, vp, vp, i32, vp]
+    L.fvb_halo_shell.restype = i32
+    L.fvb_halo_shell.argtypes = [sp, vp, vp, i32, vp]
+    L.fvb_totals_haloed.restype = i32
+    L.fvb_totals_haloed.argtypes = [sp, vp, vp, vp, vp]
     L.fvb_host_pin.restype = i32
     L.fvb_host_pin.argtypes = [vp, ctypes.c_size_t]
     L.fvb_host_unpin.restype = i32

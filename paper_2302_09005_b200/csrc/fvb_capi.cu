@@ -244,6 +244,60 @@ int fvb_update_host(const fvb_spec* spec, const double* qin_h, double* qout_h, c
   return (st_h[0] | st_h[1]) ? FVB_ERR_NONPHYSICAL : FVB_OK;
 }
 
+int fvb_update_to_haloed(const fvb_spec* spec, const double* qin, double* qin_next, const double* cell_size,
+                         const double* dt, double* max_eig, uint32_t* status, int zero_status, void* stream) {
+  int rc = check_spec(spec);
+  if (rc) return rc;
+  if (spec->n_patches == 0) return FVB_OK;
+  if (spec->dim != 2 || spec->layout != 0 || !fvb_fused2d_warp_supported(spec->p))
+    return set_contract("update_to_haloed: 2D AoS batches with 2 <= p <= 32");
+  if (!qin || !qin_next || !cell_size || !dt || !max_eig || !status || qin == qin_next)
+    return set_contract("update_to_haloed: null or aliased buffer");
+  cudaStream_t st = as_stream(stream);
+  cudaError_t e = cudaSuccess;
+  if (zero_status) e = cudaMemsetAsync(status, 0, 2 * sizeof(uint32_t), st);
+  if (e != cudaSuccess) return set_cuda_error(e, "memset status");
+  FvbArgs a;
+  a.dim = 2;
+  a.p = spec->p;
+  a.layout = 0;
+  a.n = spec->n_patches;
+  a.gamma = spec->gamma;
+  a.qin = qin;
+  a.qout = qin_next;
+  a.cell_size = cell_size;
+  a.dt = dt;
+  a.max_eig = max_eig;
+  a.status = status;
+  a.out_haloed = 1;
+  e = fvb_launch_fused2d16_warp(a, st);
+  if (e == cudaSuccess) e = fvb_launch_redo(a, st);
+  return e == cudaSuccess ? FVB_OK : set_cuda_error(e, "fvb_update_to_haloed");
+}
+
+int fvb_halo_shell(const fvb_spec* spec, double* qin, const int32_t* grid_shape, int periodic, void* stream) {
+  int rc = check_spec(spec);
+  if (rc) return rc;
+  if (spec->dim != 2 || spec->layout != 0) return set_contract("halo_shell: 2D AoS batches");
+  if (!grid_shape || grid_shape[0] < 1 || grid_shape[1] < 1 ||
+      (int64_t)grid_shape[0] * grid_shape[1] != spec->n_patches)
+    return set_contract("grid shape does not match the patch count");
+  if (spec->n_patches == 0) return FVB_OK;
+  const int g[2] = {grid_shape[0], grid_shape[1]};
+  cudaError_t e = fvb_launch_halo_shell2d(spec->p, spec->n_patches, qin, g, periodic, as_stream(stream));
+  return e == cudaSuccess ? FVB_OK : set_cuda_error(e, "fvb_halo_shell");
+}
+
+int fvb_totals_haloed(const fvb_spec* spec, const double* qin, double* scratch, double* totals, void* stream) {
+  int rc = check_spec(spec);
+  if (rc) return rc;
+  if (spec->layout != 0) return set_contract("totals_haloed: AoS batches");
+  if (spec->n_patches == 0) return set_contract("totals over an empty batch");
+  cudaError_t e = fvb_launch_totals_haloed(spec->dim, spec->p, spec->n_patches, qin, scratch, totals,
+                                           as_stream(stream));
+  return e == cudaSuccess ? FVB_OK : set_cuda_error(e, "fvb_totals_haloed");
+}
+
 int fvb_host_pin(const void* p, size_t bytes) {
   if (!p || bytes == 0) return set_contract("null host range");
   cudaPointerAttributes at;

@@ -106,7 +106,7 @@ __global__ void __launch_bounds__(WPC * 32, 4)
 fused2d_warp_kernel(const double* __restrict__ qin, double* __restrict__ qout, const double* __restrict__ cell_size,
                     const double* __restrict__ dtv, double* __restrict__ max_eig, unsigned* __restrict__ status,
                     int64_t n, Closure cl, const __grid_constant__ CUtensorMap tmap,
-                    const __grid_constant__ CUtensorMap omap) {
+                    const __grid_constant__ CUtensorMap omap, int out_haloed) {
   using C = W2<P>;
   constexpr int E = C::E, PPW = C::PPW, ROWD = C::ROWD, OFFB = C::OFFB, STGD = C::STGD, NS = C::NS, HB = C::HB;
   constexpr int XSD = C::XSD, HXR = C::HXR, HXC = C::HXC, OUTR = C::OUTR, OFFO = C::OFFO;
@@ -348,7 +348,10 @@ fused2d_warp_kernel(const double* __restrict__ qin, double* __restrict__ qout, c
           fence_proxy_async();
           __syncwarp();
           if (l == 0) {
-            tma_store_3d(&omap, 0, z0, (int)pa, outb);
+            // out_haloed: the rows land in the interior of a haloed batch (row z0+1, inner
+            // offset S doubles = 32 B); for odd P the box's second row hits the upper halo
+            // row, which the shell fill (fvb_halo_shell) rewrites afterwards
+            tma_store_3d(&omap, out_haloed ? S : 0, z0 + out_haloed, (int)pa, outb);
             bulk_commit();
           }
         }
@@ -417,8 +420,11 @@ cudaError_t make_qout_map(const FvbArgs& a, CUtensorMap* tm) {
   using C = W2<P>;
   EncodeTiledFn enc = encode_tiled();
   if (!enc) return cudaErrorNotSupported;
-  const cuuint64_t dims[3] = {(cuuint64_t)C::OUTR, (cuuint64_t)P, (cuuint64_t)a.n};
-  const cuuint64_t strides[2] = {(cuuint64_t)C::OUTR * 8, (cuuint64_t)C::OUTR * P * 8};
+  // out_haloed: the output tensor is the haloed batch {row of E volumes, E rows, patches}
+  const cuuint64_t dims[3] = {(cuuint64_t)(a.out_haloed ? C::ROWD : C::OUTR), (cuuint64_t)(a.out_haloed ? C::E : P),
+                              (cuuint64_t)a.n};
+  const cuuint64_t strides[2] = {(cuuint64_t)(a.out_haloed ? C::ROWD : C::OUTR) * 8,
+                                 (cuuint64_t)(a.out_haloed ? C::ROWD * C::E : C::OUTR * P) * 8};
   const cuuint32_t box[3] = {(cuuint32_t)C::OUTR, 2u, (cuuint32_t)C::PPW};
   const cuuint32_t es[3] = {1u, 1u, 1u};
   const CUresult r = enc(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, a.qout, dims, strides, box, es,
@@ -449,7 +455,7 @@ cudaError_t launch(const FvbArgs& a, cudaStream_t st) {
   if (e == cudaSuccess) e = make_qout_map<P>(a, &om);
   if (e != cudaSuccess) return e;
   kfn<<<(unsigned)grid, WPC * 32, BYTES, st>>>(a.qin, a.qout, a.cell_size, a.dt, a.max_eig, a.status, a.n, cl, tm,
-                                               om);
+                                               om, a.out_haloed);
   return cudaGetLastError();
 }
 }  // namespace f2w

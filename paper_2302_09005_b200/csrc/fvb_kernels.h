@@ -21,6 +21,7 @@ struct FvbArgs {
   const double* dt;
   double* max_eig;
   unsigned* status;
+  int out_haloed = 0;   // 1: qout is a haloed AoS batch (N*V*S); the update fills its interior
 };
 
 cudaError_t fvb_launch_generic(const FvbArgs& a, cudaStream_t st);
@@ -62,5 +63,8 @@ bool fvb_halo_window_supported(int dim, int p);
 cudaError_t fvb_launch_halo_window(int dim, int p, int64_t n, const double* ghost_lo, const double* qout,
                                    const double* ghost_hi, double* qin, const int* window_grid, int nlo, int pmask,
                                    double* scratch, double* totals, cudaStream_t st);
+cudaError_t fvb_launch_halo_shell2d(int p, int64_t n, double* q, const int* grid, int periodic, cudaStream_t st);
+cudaError_t fvb_launch_totals_haloed(int dim, int p, int64_t n, const double* q, double* scratch, double* totals,
+                                     cudaStream_t st);
 cudaError_t fvb_launch_totals(int dim, int p, int64_t n, int layout, const double* qout, double* scratch,
                               double* totals, cudaStream_t st);

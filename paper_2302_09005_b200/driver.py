@@ -171,6 +171,35 @@ def run_simulation(db: DeviceBatch, grid_shape, steps: int, cfl: float = 0.4, pe
     k_t = torch.zeros(1, dtype=torch.int64, device=dev)    # device step counter (graph mode)
     tot_cur = torch.empty(s, **f64)
 
+    # 2D AoS fast path: the update writes into the interior of the other haloed buffer,
+    # then only its halo shell is filled (fvb_update_to_haloed / fvb_halo_shell)
+    import os
+
+    p = db.spec.volumes_per_axis
+    direct = (db.spec.dimensions == 2 and db.layout == "aos" and 2 <= p <= 32 and kernel in ("auto", "fused")
+              and os.environ.get("FVB_RUNSIM_DIRECT", "1") != "0")
+    bufs = [db.QIn, torch.empty_like(db.QIn)] if direct else None
+    gshape = (ctypes.c_int32 * 3)(*(list(grid_shape) + [1] * (3 - len(grid_shape))))
+
+    def direct_step(k):
+        from .device import _stream_handle as _sh
+
+        L = _lib.load()
+        fs = ctypes.byref(db.fvb_spec())
+        st = _sh(torch, None)
+        src, dst = bufs[k % 2], bufs[(k + 1) % 2]
+        dt_h.index_copy_(0, k_t, stepper.dt_scalar)
+        db.status[1:2].zero_()
+        _lib.check(L.fvb_update_to_haloed(fs, _vp(src), _vp(dst), _vp(db.cell_size), _vp(db.dt),
+                                          _vp(db.max_eigenvalue), _vp(db.status), 0, st), "fvb_update_to_haloed")
+        flag_h.index_copy_(0, k_t, db.status[0:1])
+        stepper.reduce_dt()
+        _lib.check(L.fvb_halo_shell(fs, _vp(dst), gshape, int(bool(periodic)), st), "fvb_halo_shell")
+        _lib.check(L.fvb_totals_haloed(fs, _vp(dst), _vp(scratch), _vp(tot_cur), st), "fvb_totals_haloed")
+        k_t.add_(1)
+        tot_h.index_copy_(0, k_t, tot_cur[None])
+        gmax_h.index_copy_(0, k_t, stepper.gmax)
+
     def step_body():
         dt_h.index_copy_(0, k_t, stepper.dt_scalar)       # the dt this step advances by
         db.status[1:2].zero_()                            # redo count of this launch; status[0] accumulates
@@ -185,7 +214,17 @@ def run_simulation(db: DeviceBatch, grid_shape, steps: int, cfl: float = 0.4, pe
     g = None
     if graph is None:
         graph = steps >= 64
-    if graph and steps > 1:
+    if direct:
+        for k in range(steps):
+            direct_step(k)
+        final = bufs[steps % 2]
+        e = p + 2
+        n = db.n_patches
+        db.QOut.view(n, p, p, 4).copy_(final.view(n, e, e, 4)[:, 1:-1, 1:-1, :])
+        if final is not db.QIn:
+            db.QIn.copy_(final)
+        graph = False
+    elif graph and steps > 1:
         try:
             side = torch.cuda.Stream(device=dev)
             side.wait_stream(torch.cuda.current_stream(dev))
@@ -198,7 +237,7 @@ def run_simulation(db: DeviceBatch, grid_shape, steps: int, cfl: float = 0.4, pe
     if g is not None:
         for _ in range(steps):
             g.replay()
-    else:
+    elif not direct:
         for _ in range(steps):
             step_body()
 

@@ -1,4 +1,5 @@
-"""Wall time per step of driver.run_simulation on a 16^3 grid of 3D p=16 patches (4,096 patches).
+"""Wall time per step of driver.run_simulation on a 16^3 grid of 3D p=16 patches (4,096 patches),
+or with --2d on a 256^2 grid of 2D p=16 patches (65,536 patches, C2's batch).
 
     python scripts/time_runsim.py          # moving fluid with a random density perturbation
     python scripts/time_runsim.py --sod    # Sod shock tube along x: fluid at rest (exact +0 momentum)
@@ -13,20 +14,22 @@ import torch
 sys.path.insert(0, ".")
 from paper_2302_09005_b200 import device, driver, mesh, pde  # noqa: E402
 
-g, p = (16, 16, 16), 16
+dim = 2 if "--2d" in sys.argv else 3
+g, p = ((256, 256) if dim == 2 else (16, 16, 16)), 16
 n = int(np.prod(g))
-spec = mesh.PatchSpec(3, p, 5)
+spec = mesh.PatchSpec(dim, p, dim + 2)
 db = device.DeviceBatch(spec, n, 1.4)
-q = db.QOut.view(n, p ** 3, 5)
+q = db.QOut.view(n, p ** dim, dim + 2)
+vel0 = [0.0, 0.0, 0.0][:dim]
 if "--sod" in sys.argv:
-    left = torch.tensor(pde.euler_state(1.0, [0.0, 0.0, 0.0], 1.0), dtype=torch.float64, device="cuda")
-    right = torch.tensor(pde.euler_state(0.125, [0.0, 0.0, 0.0], 0.1), dtype=torch.float64, device="cuda")
+    left = torch.tensor(pde.euler_state(1.0, vel0, 1.0), dtype=torch.float64, device="cuda")
+    right = torch.tensor(pde.euler_state(0.125, vel0, 0.1), dtype=torch.float64, device="cuda")
     px = torch.arange(n, device="cuda") % g[0]               # patch x index (x fastest)
     q[...] = torch.where((px < g[0] // 2)[:, None, None], left, right)
 else:
-    state = torch.tensor(pde.euler_state(1.0, [0.2, 0.1, -0.1], 1.0), dtype=torch.float64, device="cuda")
+    state = torch.tensor(pde.euler_state(1.0, [0.2, 0.1, -0.1][:dim], 1.0), dtype=torch.float64, device="cuda")
     q[...] = state
-    q[:, :, 0] += 0.1 * torch.rand(n, p ** 3, device="cuda", dtype=torch.float64)
+    q[:, :, 0] += 0.1 * torch.rand(n, p ** dim, device="cuda", dtype=torch.float64)
 db.cell_size.fill_(1.0 / 16)
 driver.run_simulation(db, g, steps=2, graph="--eager" not in sys.argv)
 torch.cuda.synchronize()
@@ -36,4 +39,5 @@ for steps in (10, 40, 200):
     res = driver.run_simulation(db, g, steps=steps, graph=graph)
     torch.cuda.synchronize()
     dt = time.perf_counter() - t0
-    print(f"run_simulation {steps} steps: {dt / steps * 1e3:.3f} ms/step, {n * p**3 * steps / dt / 1e9:.2f} Gcell/s")
+    print(f"run_simulation {dim}D {steps} steps: {dt / steps * 1e3:.3f} ms/step, "
+          f"{n * p**dim * steps / dt / 1e9:.2f} Gcell/s")

@@ -264,3 +264,24 @@ def test_run_simulation_graph_matches_eager(dim, p, grid):
     assert_bits_equal(dbs[1].QOut.cpu().numpy(), dbs[0].QOut.cpu().numpy(), "QOut")
     assert res[1].dt == res[0].dt and res[1].max_eigenvalue == res[0].max_eigenvalue
     assert_bits_equal(np.asarray(res[1].totals), np.asarray(res[0].totals), "totals")
+
+
+@pytest.mark.parametrize("p,grid,periodic", [(16, (4, 5), True), (16, (3, 3), False), (17, (3, 4), True),
+                                             (5, (6, 2), False), (32, (2, 2), True), (3, (1, 1), True)])
+def test_run_simulation_2d_direct_path_matches(p, grid, periodic, monkeypatch):
+    """2D run_simulation's fast path (update straight into the next haloed batch + halo shell)
+    gives the classic path's field, QIn, dt history and wave speeds bit for bit."""
+    dim = 2
+    n = int(np.prod(grid))
+    q = oracle.synthetic_qin(dim, p, n, seed=33 + p).reshape(n, p + 2, p + 2, dim + 2)
+    interior = q[:, 1:-1, 1:-1, :].reshape(n, -1)
+    out = {}
+    for direct in ("0", "1"):
+        monkeypatch.setenv("FVB_RUNSIM_DIRECT", direct)
+        db = _db_with_field(dim, p, grid, interior)
+        res = driver.run_simulation(db, grid, steps=5, cfl=0.4, periodic=periodic)
+        out[direct] = (db.QOut.cpu().numpy(), db.QIn.cpu().numpy(), res)
+    assert_bits_equal(out["1"][0], out["0"][0], "QOut")
+    assert_bits_equal(out["1"][1], out["0"][1], "QIn (final halo)")
+    assert out["1"][2].dt == out["0"][2].dt and out["1"][2].max_eigenvalue == out["0"][2].max_eigenvalue
+    np.testing.assert_allclose(np.asarray(out["1"][2].totals), np.asarray(out["0"][2].totals), rtol=1e-13)
