@@ -56,6 +56,25 @@ def test_capi_contract_checks_without_gpu():
     assert L.fvb_select_kernel(ctypes.byref(_lib.spec(2, 33, 5, 1.4))) == _lib.KERNEL_GENERIC
     assert L.fvb_select_kernel(ctypes.byref(_lib.spec(2, 17, 5, 1.4, 1))) == _lib.KERNEL_GENERIC
     assert L.fvb_update_host_workspace(ctypes.byref(_lib.spec(3, 16, 8, 1.4)), 4) > 4 * 233280 * 2
+    # entry points added for run_simulation / multi-GPU / host pinning: contract checks first
+    C = _lib.FVB_ERR_CONTRACT
+    g2 = (ctypes.c_int32 * 3)(2, 3, 1)
+    assert L.fvb_update_to_haloed(ctypes.byref(_lib.spec(3, 16, 4, 1.4)), None, None, None, None, None, None, 0,
+                                  None) == C                                      # 3D: no fast path
+    assert L.fvb_update_to_haloed(ctypes.byref(_lib.spec(2, 33, 4, 1.4)), None, None, None, None, None, None, 0,
+                                  None) == C                                      # p > 32
+    assert L.fvb_update_to_haloed(ctypes.byref(_lib.spec(2, 16, 4, 1.4)), None, None, None, None, None, None, 0,
+                                  None) == C                                      # null buffers
+    assert L.fvb_halo_shell(ctypes.byref(_lib.spec(2, 16, 5, 1.4)), None, g2, 1, None) == C   # 2x3 != 5 patches
+    assert L.fvb_halo_shell(ctypes.byref(_lib.spec(3, 16, 6, 1.4)), None, g2, 1, None) == C   # 3D
+    assert L.fvb_totals_haloed(ctypes.byref(_lib.spec(2, 16, 0, 1.4)), None, None, None, None) == C
+    assert L.fvb_halo_project_window(ctypes.byref(_lib.spec(2, 40, 4, 1.4)), None, None, None, None, g2, 0, 0,
+                                     None, None, None) == C                       # p > 32
+    assert L.fvb_halo_project_window(ctypes.byref(_lib.spec(2, 16, 5, 1.4)), None, None, None, None, g2, 0, 0,
+                                     None, None, None) == C                       # not whole layers
+    assert L.fvb_mgpu_init(0, None) == C
+    assert L.fvb_mgpu_allreduce_max(0, None, None) == C
+    assert L.fvb_host_pin(None, 0) == C
 
 
 def test_validation_order_matches_reference():
