@@ -136,6 +136,25 @@ class DeviceBatch:
             _vp(self.max_eigenvalue), _vp(self.status), kernel_id(kernel), int(zero_status),
             _stream_handle(torch, stream)), "fvb_update")
 
+    def update_range(self, p0: int, p1: int, kernel="auto", stream=None) -> None:
+        """The update of patches [p0, p1) only (a contiguous sub-batch: same buffers, offset
+        pointers; the status flag accumulates, the redo count is reset for this launch).
+        run_simulation_sharded updates its boundary layers first with it, so their exchange
+        overlaps the update of the interior layers."""
+        torch = _torch()
+        if not (0 <= p0 < p1 <= self.n_patches):
+            raise ContractViolationError(f"patch range [{p0}, {p1}) outside the batch of {self.n_patches}")
+        d, s = self.spec.dimensions, self.spec.unknowns
+        V, I = self.spec.haloed_volumes, self.spec.interior_volumes
+        sub = _lib.spec(d, self.spec.volumes_per_axis, p1 - p0, self.gamma, LAYOUTS[self.layout])
+        if self.layout != "aos":
+            raise ContractViolationError("update_range: AoS batches only")
+        self.status[1:2].zero_()
+        _lib.check(_lib.load().fvb_update(
+            ctypes.byref(sub), _vp(self.QIn[p0 * V * s:]), _vp(self.QOut[p0 * I * s:]),
+            _vp(self.cell_size[p0 * d:]), _vp(self.dt[p0:]), _vp(self.max_eigenvalue[p0:]), _vp(self.status),
+            kernel_id(kernel), 0, _stream_handle(torch, stream)), "fvb_update")
+
     def max_eig_prepass(self, stream=None) -> None:
         """Per-patch wave speed of QIn without an update (first-step dt)."""
         torch = _torch()

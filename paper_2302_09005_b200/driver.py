@@ -266,6 +266,13 @@ def _neighbours(rank: int, world: int, periodic: bool):
 
 def exchange_ghost_layers(own, layer_elems: int, ghost_lo, ghost_hi, rank: int, world: int, periodic: bool,
                           group=None) -> None:
+    """Blocking form of exchange_ghost_layers_start (see there)."""
+    for w in exchange_ghost_layers_start(own, layer_elems, ghost_lo, ghost_hi, rank, world, periodic, group):
+        w.wait()
+
+
+def exchange_ghost_layers_start(own, layer_elems: int, ghost_lo, ghost_hi, rank: int, world: int, periodic: bool,
+                                group=None) -> list:
     """Fill ghost_lo with the lower neighbour's last layer and ghost_hi with the upper
     neighbour's first layer (flat tensors; `own` holds whole layers of layer_elems values).
 
@@ -273,7 +280,8 @@ def exchange_ghost_layers(own, layer_elems: int, ghost_lo, ghost_hi, rank: int, 
     issued in one fixed order on every rank -- [send last -> upper, send first -> lower,
     recv lower, recv upper] -- so that with two ranks, where the lower and upper
     neighbour are the same rank, the k-th message between a pair still lands in the
-    right buffer.  A single periodic rank copies its own layers."""
+    right buffer.  A single periodic rank copies its own layers.  Returns the pending
+    requests (wait on them before reading the ghosts)."""
     lo, hi = _neighbours(rank, world, periodic)
     first, last = own[:layer_elems], own[own.numel() - layer_elems:]
     if world == 1:
@@ -281,7 +289,7 @@ def exchange_ghost_layers(own, layer_elems: int, ghost_lo, ghost_hi, rank: int, 
             ghost_lo.copy_(last)
         if hi is not None:
             ghost_hi.copy_(first)
-        return
+        return []
     import torch.distributed as dist
 
     ops = []
@@ -293,8 +301,7 @@ def exchange_ghost_layers(own, layer_elems: int, ghost_lo, ghost_hi, rank: int, 
         ops.append(dist.P2POp(dist.irecv, ghost_lo, lo, group))
     if hi is not None:
         ops.append(dist.P2POp(dist.irecv, ghost_hi, hi, group))
-    for w in dist.batch_isend_irecv(ops):
-        w.wait()
+    return dist.batch_isend_irecv(ops)   # the caller waits (after overlapping work, if any)
 
 
 def shard_layout(grid_shape, rank: int, world: int, periodic: bool) -> dict:
@@ -358,6 +365,29 @@ class ShardedGrid:
         exchange_ghost_layers(self.db.QOut, self.layer_elems, self.ghost_lo, self.ghost_hi, self.rank, self.world,
                               self.periodic, self.group)
 
+    def update_and_exchange(self, kernel="auto") -> None:
+        """The step's update with the ghost exchange overlapped: the two boundary layers are
+        updated first and sent while the interior layers update (NCCL runs on its own stream,
+        ordered after the boundary launches; the ghosts are awaited before the halo)."""
+        own_layers = self.l1 - self.l0
+        if self.world == 1 or own_layers < 3 or self.db.layout != "aos":
+            self.db.update(kernel=kernel, zero_status=False)
+            self.exchange()
+            return
+        L, n = self.layer, self.db.n_patches
+        self.db.update_range(0, L, kernel)
+        self.db.update_range(n - L, n, kernel)
+        works = exchange_ghost_layers_start(self.db.QOut, self.layer_elems, self.ghost_lo, self.ghost_hi, self.rank,
+                                            self.world, self.periodic, self.group)
+        self.db.update_range(L, n - L, kernel)
+        for w in works:
+            w.wait()
+
+    def halo_only(self, totals_out=None, scratch=None) -> None:
+        """This shard's QIn from its own layers and the (already exchanged) ghosts."""
+        self.db.halo_project_window(self.window_grid, self.lo_layers, self.ghost_lo, self.ghost_hi, self.pmask,
+                                    totals_out, scratch)
+
     def halo(self, totals_out=None, scratch=None) -> None:
         """Ghost exchange, then this shard's QIn (and its local totals if totals_out is given)."""
         self.exchange()
@@ -369,7 +399,8 @@ def run_simulation_sharded(sg: ShardedGrid, steps: int, cfl: float = 0.4, kernel
                            dx: float | None = None) -> SimulationResult:
     """run_simulation over a grid sharded across ranks (one GPU each): the same step --
     dt from the global maximum wave speed (one MAX all-reduce), fused update of the own
-    patches, then the ghost-layer exchange and the windowed halo projection.  Totals are
+    patches (the two boundary layers first, so their ghost-layer exchange overlaps the
+    update of the interior layers), then the windowed halo projection.  Totals are
     summed over ranks in rank order.  With one rank it reproduces run_simulation bit for bit
     (the exchange is a local copy)."""
     import numpy as np
@@ -386,8 +417,11 @@ def run_simulation_sharded(sg: ShardedGrid, steps: int, cfl: float = 0.4, kernel
     scratch = db.totals_scratch()
     multi = sg.world > 1
 
-    def halo_and_totals(k):
-        sg.halo(tot_h[k], scratch)
+    def halo_and_totals(k, exchanged=False):
+        if exchanged:
+            sg.halo_only(tot_h[k], scratch)
+        else:
+            sg.halo(tot_h[k], scratch)
         if multi:   # global totals: gather the shards' vectors, sum in rank order (deterministic)
             parts = [torch.empty(s, **f64) for _ in range(sg.world)]
             dist.all_gather(parts, tot_h[k].contiguous(), group=sg.group)
@@ -404,10 +438,10 @@ def run_simulation_sharded(sg: ShardedGrid, steps: int, cfl: float = 0.4, kernel
     for k in range(steps):
         dt_h[k].copy_(stepper.dt_scalar[0])
         db.status[1:2].zero_()
-        db.update(kernel=kernel, zero_status=False)
+        sg.update_and_exchange(kernel)        # boundary layers first, their exchange overlaps the rest
         flag_h[k].copy_(db.status[0])
         stepper.reduce_dt()
-        halo_and_totals(k + 1)
+        halo_and_totals(k + 1, exchanged=True)
         gmax_h[k + 1].copy_(stepper.gmax[0])
 
     flags = flag_h.clone()

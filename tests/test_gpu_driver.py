@@ -285,3 +285,30 @@ def test_run_simulation_2d_direct_path_matches(p, grid, periodic, monkeypatch):
     assert_bits_equal(out["1"][1], out["0"][1], "QIn (final halo)")
     assert out["1"][2].dt == out["0"][2].dt and out["1"][2].max_eigenvalue == out["0"][2].max_eigenvalue
     np.testing.assert_allclose(np.asarray(out["1"][2].totals), np.asarray(out["0"][2].totals), rtol=1e-13)
+
+
+@pytest.mark.parametrize("dim,p,grid", [(3, 16, (2, 2, 5)), (2, 16, (3, 7)), (3, 4, (2, 3, 4))])
+def test_update_range_split_matches_whole(dim, p, grid, monkeypatch):
+    """ShardedGrid.update_and_exchange's split update (first layer, last layer, then the
+    interior layers, the exchange started in between) equals one whole update bit for bit."""
+    n = int(np.prod(grid))
+    spec = mesh.PatchSpec(dim, p, dim + 2)
+    qin = oracle.synthetic_qin(dim, p, n, seed=77)
+    b = mesh.make_patch_batch(spec, n)
+    b.QIn[...] = qin
+    b.dt[...] = 0.4 / p / 3.4
+    whole = device.DeviceBatch.from_host(b, 1.4)
+    whole.update()
+    calls = []
+    monkeypatch.setattr(driver, "exchange_ghost_layers_start", lambda *a, **k: calls.append(1) or [])
+    sg = driver.ShardedGrid(spec, grid, 1.4, True, rank=1, world=3)   # a middle rank: both ghosts
+    lay = driver.shard_layout(grid, 1, 3, True)
+    sg.db.QIn.copy_(whole.QIn.view(n, -1)[lay["patch_lo"]:lay["patch_hi"]].reshape(-1))
+    sg.db.dt.copy_(whole.dt[lay["patch_lo"]:lay["patch_hi"]])
+    sg.db.status.zero_()
+    sg.update_and_exchange()
+    torch.cuda.synchronize()
+    assert calls == [1]
+    lo, hi = lay["patch_lo"], lay["patch_hi"]
+    assert_bits_equal(sg.db.QOut.cpu().numpy(), whole.QOut.view(n, -1)[lo:hi].reshape(-1).cpu().numpy(), "QOut")
+    assert_bits_equal(sg.db.max_eigenvalue.cpu().numpy(), whole.max_eigenvalue[lo:hi].cpu().numpy(), "max_eig")
