@@ -92,3 +92,31 @@ def test_criterion_8_schedule_independence():
             db.halo_project_totals(grid, True, tot, scratch)
         assert not db.nonphysical()
         assert np.array_equal(db.QOut.cpu().numpy().view(np.uint64), ref.QOut.cpu().numpy().view(np.uint64)), N
+
+
+@pytest.mark.parametrize("dim,p", [(2, 17), (3, 16), (3, 4), (2, 5)])
+def test_criterion_6_eigenvalue_reduction(dim, p):
+    """SPEC.md:563 #6: per-patch max_eigenvalue equals the brute-force max over the interior
+    volumes' directional eigenvalues |j_n / rho| + sqrt(gamma p / rho) (numpy, pde.py:62-70
+    operation order), exactly, on 100 random patches."""
+    import oracle
+
+    n, g = 100, 1.4
+    spec = mesh.PatchSpec(dim, p, dim + 2)
+    b = mesh.make_patch_batch(spec, n)
+    b.QIn[...] = oracle.synthetic_qin(dim, p, n, seed=600 + p)
+    b.dt[...] = 0.4 / p / 3.4
+    db = device.DeviceBatch.from_host(b, g)
+    db.update()
+    lam = db.max_eigenvalue.cpu().numpy()
+    e = p + 2
+    q = b.QIn.reshape((n,) + (e,) * dim + (dim + 2,))
+    q = q[(slice(None),) + (slice(1, -1),) * dim].reshape(n, -1, dim + 2)
+    rho = q[..., 0]
+    mom2 = q[..., 1] * q[..., 1]
+    for a in range(2, dim + 1):
+        mom2 = mom2 + q[..., a] * q[..., a]
+    pr = (g - 1.0) * (q[..., -1] - (0.5 * mom2) / rho)
+    c = np.sqrt((g * pr) / rho)
+    brute = np.max(np.stack([np.abs(q[..., 1 + k] / rho) + c for k in range(dim)], axis=-1), axis=(1, 2))
+    assert np.array_equal(lam.view(np.uint64), brute.view(np.uint64))
