@@ -39,7 +39,7 @@ extern "C" {
 /* kernel selector for fvb_update / fvb_update_host */
 #define FVB_KERNEL_AUTO 0     /* the shape's fused kernel when it has one, else generic */
 #define FVB_KERNEL_GENERIC 1  /* any d, p */
-#define FVB_KERNEL_FUSED 2    /* 2D/3D p == 16 (AoS or SoA), 3D even p == 2..8 (AoS), 2D p == 2..32 (AoS) */
+#define FVB_KERNEL_FUSED 2    /* 2D/3D p == 16 (AoS or SoA), 3D p == 2, 4..8 (AoS), 2D p == 2..32 (AoS) */
 
 typedef struct fvb_spec {
   int32_t dim;       /* PatchSpec.dimensions (mesh.py:29), 2 or 3 */
