@@ -237,3 +237,20 @@ def test_shard_layout_covers_grid_with_ghosts():
                     assert lay["pmask"] == (((1 << (len(grid) - 1)) - 1) if periodic else 0)
                     assert lay["patch_hi"] - lay["patch_lo"] == (lay["l1"] - lay["l0"]) * lay["layer"]
                 assert prev == grid[-1]
+
+
+def test_c_host_demo_compiles():
+    """examples/c_host_demo.c builds against include/fvb200.h and links libfvb200.so with a
+    plain C compiler (no Python / torch types on the boundary); it runs on the GPU box
+    (tests/test_gpu_c_host.py)."""
+    import shutil
+    import subprocess
+
+    import pytest
+
+    if shutil.which("gcc") is None or shutil.which("make") is None:  # pragma: no cover
+        pytest.skip("no C toolchain")
+    ex = os.path.join(ROOT, "examples")
+    r = subprocess.run(["make", "-s", "-B", "-C", ex], capture_output=True, text=True, timeout=120)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert os.path.exists(os.path.join(ex, "c_host_demo"))
