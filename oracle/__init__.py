@@ -143,12 +143,12 @@ def synthetic_qin(dim: int, p: int, n: int, seed: int = 0, gamma: float = 1.4) -
     return q.reshape(n, v * (dim + 2))
 
 
-def halo_project(dim: int, p: int, qout: np.ndarray, grid, periodic: bool) -> np.ndarray:
+def halo_project(dim: int, p: int, qout: np.ndarray, grid, periodic: bool, s: int | None = None) -> np.ndarray:
     """Restatement of mesh.halo_project (mesh.py:261-310) as index arithmetic (numpy):
     haloed QIn of every patch from the grid's interior QOut, per-axis wrap / clamp."""
     grid = tuple(int(g) for g in grid)
     n = int(np.prod(grid))
-    s = dim + 2
+    s = dim + 2 if s is None else s
     e = p + 2
     qo = np.asarray(qout).reshape(n, p ** dim, s)
     qin = np.empty((n, e ** dim, s))

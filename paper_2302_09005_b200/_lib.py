@@ -135,8 +135,9 @@ def load():
     return L
 
 
-def spec(dim: int, p: int, n: int, gamma: float, layout: int = 0) -> FvbSpec:
-    return FvbSpec(dim, p, dim + 2, layout, n, gamma)
+def spec(dim: int, p: int, n: int, gamma: float, layout: int = 0, unknowns: int | None = None) -> FvbSpec:
+    """C-ABI spec; `unknowns` defaults to the Euler count d + 2 (only fvb_halo_project accepts others)."""
+    return FvbSpec(dim, p, dim + 2 if unknowns is None else unknowns, layout, n, gamma)
 
 
 def check(rc: int, what: str) -> None:

@@ -388,8 +388,17 @@ int fvb_selftest_div(const double* a, const double* b, double* out_shared, doubl
 
 int fvb_halo_project(const fvb_spec* spec, const double* qout, double* qin, const int32_t* grid_shape,
                      int periodic, void* stream) {
-  int rc = check_spec(spec);
-  if (rc) return rc;
+  // Pure data movement: any unknown count s >= 1 (the reference's halo_project
+  // works for every PatchSpec); only the Euler shape s = d + 2 has the fast kernels.
+  if (spec && spec->unknowns >= 1 && spec->unknowns != spec->dim + 2) {
+    fvb_spec euler = *spec;
+    euler.unknowns = spec->dim + 2;
+    int rc0 = check_spec(&euler);
+    if (rc0) return rc0;
+  } else {
+    int rc = check_spec(spec);
+    if (rc) return rc;
+  }
   if (!grid_shape) return set_contract("null grid shape");
   int64_t cells = 1;
   for (int a = 0; a < spec->dim; ++a) {
@@ -398,8 +407,12 @@ int fvb_halo_project(const fvb_spec* spec, const double* qout, double* qin, cons
   }
   if (cells != spec->n_patches) return set_contract("grid shape does not match the patch count");
   if (spec->n_patches == 0) return FVB_OK;
-  cudaError_t e = fvb_launch_halo_project(spec->dim, spec->p, spec->n_patches, spec->layout, qout, qin,
-                                          grid_shape, periodic, as_stream(stream));
+  cudaError_t e = spec->unknowns == spec->dim + 2
+                      ? fvb_launch_halo_project(spec->dim, spec->p, spec->n_patches, spec->layout, qout, qin,
+                                                grid_shape, periodic, as_stream(stream))
+                      : fvb_launch_halo_project_any_s(spec->dim, spec->p, spec->unknowns, spec->n_patches,
+                                                      spec->layout, qout, qin, grid_shape, periodic,
+                                                      as_stream(stream));
   return e == cudaSuccess ? FVB_OK : set_cuda_error(e, "fvb_halo_project");
 }
 

@@ -54,6 +54,8 @@ cudaError_t fvb_launch_probe(int dim, double gamma, const double* states, int64_
 bool fvb_halo_tma_supported(int dim, int p);
 cudaError_t fvb_launch_halo_tma(int dim, int p, int64_t n, const double* qout, double* qin, const int* grid,
                                 int periodic, cudaStream_t st);
+cudaError_t fvb_launch_halo_project_any_s(int dim, int p, int s, int64_t n, int layout, const double* qout,
+                                          double* qin, const int* grid, int periodic, cudaStream_t st);
 cudaError_t fvb_launch_halo_project(int dim, int p, int64_t n, int layout, const double* qout, double* qin,
                                     const int* grid, int periodic, cudaStream_t st);
 cudaError_t fvb_launch_halo_project_totals(int dim, int p, int64_t n, int layout, const double* qout, double* qin,

@@ -389,7 +389,7 @@ def halo_project_host(batch: PatchBatch, grid_shape, periodic: bool, device=None
     with torch.cuda.device(dev):
         qout = torch.from_numpy(np.ascontiguousarray(batch.QOut, dtype=np.float64).reshape(-1)).to(dev)
         qin = torch.empty(batch.n_patches * spec.haloed_volumes * spec.unknowns, dtype=torch.float64, device=dev)
-        fs = _lib.spec(spec.dimensions, spec.volumes_per_axis, batch.n_patches, 1.4, 0)
+        fs = _lib.spec(spec.dimensions, spec.volumes_per_axis, batch.n_patches, 1.4, 0, unknowns=spec.unknowns)
         g = (ctypes.c_int32 * 3)(*(list(grid_shape) + [1] * (3 - len(grid_shape))))
         _lib.check(_lib.load().fvb_halo_project(ctypes.byref(fs), _vp(qout), _vp(qin), g, int(bool(periodic)),
                                                 _stream_handle(torch, None)), "fvb_halo_project")

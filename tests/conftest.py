@@ -43,3 +43,24 @@ def assert_bits_equal(a, b, what=""):
         idx = np.argwhere(~same)[:5]
         details = [(tuple(i), a[tuple(i)], b[tuple(i)]) for i in idx]
         raise AssertionError(f"{what}: {int((~same).sum())} elements differ bitwise, e.g. {details}")
+
+
+def import_reference():
+    """The reference package `fvbatch`, or None.
+
+    Looked up in baseline/_ref (the offline pip install of /root/reference,
+    git-ignored but shipped to the GPU box with the snapshot) and then in
+    /root/reference/pkg/src (this container only).  Tests use it as the
+    caller side of the drop-in and as a second checker; the product package
+    never imports it."""
+    import importlib
+
+    for path in (os.path.join(ROOT, "baseline", "_ref"), "/root/reference/pkg/src"):
+        if os.path.isdir(os.path.join(path, "fvbatch")):
+            if path not in sys.path:
+                sys.path.append(path)
+            try:
+                return importlib.import_module("fvbatch")
+            except Exception:  # pragma: no cover - broken install
+                return None
+    return None

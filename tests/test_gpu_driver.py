@@ -57,6 +57,19 @@ def test_halo_project_random_vs_oracle(dim, p, grid):
         mesh.halo_project(b, grid[:-1], True)
 
 
+@pytest.mark.parametrize("dim,p,s,grid", [(2, 4, 3, (2, 3)), (3, 1, 1, (2, 2, 2)), (3, 4, 1, (3, 1, 2)),
+                                          (2, 16, 7, (4, 2)), (3, 5, 9, (2, 1, 2)), (2, 3, 1, (1, 1))])
+def test_halo_project_any_unknown_count(dim, p, s, grid):
+    """halo_project is data movement: any s (s != d + 2 used to overrun the buffers)."""
+    n = int(np.prod(grid))
+    b = mesh.make_patch_batch(mesh.PatchSpec(dim, p, s), n)
+    b.QOut[...] = np.random.default_rng(s * 100 + n).standard_normal(b.QOut.shape)
+    for periodic in (True, False):
+        b.QIn[...] = np.nan
+        mesh.halo_project(b, grid, periodic)
+        assert_bits_equal(b.QIn, oracle.halo_project(dim, p, b.QOut, grid, periodic, s=s), f"s={s} {periodic}")
+
+
 @pytest.mark.parametrize("dim,p,grid", [(3, 16, (4, 3, 2)), (3, 4, (3, 3, 3)), (3, 5, (1, 2, 3)), (2, 16, (8, 5)),
                                         (3, 32, (1, 2, 1))])
 def test_halo_project_totals_fused(dim, p, grid):
