@@ -75,6 +75,8 @@ int fvb_update(const fvb_spec* spec, const double* qin, double* qout, const doub
   if (rc) return rc;
   if (spec->n_patches == 0) return FVB_OK;   // kernel/__init__.py:123-124
   if (!qin || !qout || !cell_size || !dt || !max_eig || !status) return set_contract("null buffer");
+  const bool fast = (kernel & FVB_MODE_FAST) != 0;
+  kernel &= ~FVB_MODE_FAST;
   const int k = resolve_kernel(spec, kernel);
   if (k == FVB_KERNEL_FUSED && !fvb_fused16_supported(spec->dim, spec->p, spec->layout))
     return set_contract("no fused kernel for this shape (2D/3D p=16, 3D even p=2..8 AoS, 2D p=2..32 AoS)");
@@ -102,6 +104,9 @@ int fvb_update(const fvb_spec* spec, const double* qin, double* qout, const doub
     e = cudaMemsetAsync(max_eig, 0, sizeof(double) * (size_t)spec->n_patches, st);
     if (e != cudaSuccess) return set_cuda_error(e, "memset max_eig");
     e = fvb_launch_generic(a, st);
+  } else if (fast && fvb_fast3d_supported(spec->dim, spec->p, spec->layout)) {
+    e = fvb_launch_fast3d16(a, st);
+    if (e == cudaSuccess) e = fvb_launch_redo(a, st);   // exact re-evaluation of queued patches
   } else {
     e = fvb_launch_fused16(a, st);
   }

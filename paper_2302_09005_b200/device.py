@@ -48,11 +48,17 @@ def _stream_handle(torch, stream) -> ctypes.c_void_p:
     return ctypes.c_void_p(s.cuda_stream)
 
 
-def kernel_id(kernel) -> int:
+MODES = {"exact": 0, "fast": 0x100}   # FVB_MODE_FAST (include/fvb200.h)
+
+
+def kernel_id(kernel, mode: str = "exact") -> int:
+    """C-ABI kernel selector; mode "fast" ORs in FVB_MODE_FAST (1e-12 relative, exact max_eig)."""
+    if mode not in MODES:
+        raise ContractViolationError(f"unknown mode {mode!r} (expected 'exact' or 'fast')")
     if isinstance(kernel, int):
-        return kernel
+        return kernel | MODES[mode]
     try:
-        return KERNELS[kernel]
+        return KERNELS[kernel] | MODES[mode]
     except KeyError:
         raise ContractViolationError(f"unknown kernel selector {kernel!r}") from None
 
@@ -128,15 +134,15 @@ class DeviceBatch:
         return out
 
     # -- compute --------------------------------------------------------------------------------
-    def update(self, kernel="auto", stream=None, zero_status: bool = True) -> None:
+    def update(self, kernel="auto", stream=None, zero_status: bool = True, mode: str = "exact") -> None:
         """One Rusanov step, asynchronous on `stream` (torch's current stream by default)."""
         torch = _torch()
         _lib.check(_lib.load().fvb_update(
             ctypes.byref(self.fvb_spec()), _vp(self.QIn), _vp(self.QOut), _vp(self.cell_size), _vp(self.dt),
-            _vp(self.max_eigenvalue), _vp(self.status), kernel_id(kernel), int(zero_status),
+            _vp(self.max_eigenvalue), _vp(self.status), kernel_id(kernel, mode), int(zero_status),
             _stream_handle(torch, stream)), "fvb_update")
 
-    def update_range(self, p0: int, p1: int, kernel="auto", stream=None) -> None:
+    def update_range(self, p0: int, p1: int, kernel="auto", stream=None, mode: str = "exact") -> None:
         """The update of patches [p0, p1) only (a contiguous sub-batch: same buffers, offset
         pointers; the status flag accumulates, the redo count is reset for this launch).
         run_simulation_sharded updates its boundary layers first with it, so their exchange
@@ -153,7 +159,7 @@ class DeviceBatch:
         _lib.check(_lib.load().fvb_update(
             ctypes.byref(sub), _vp(self.QIn[p0 * V * s:]), _vp(self.QOut[p0 * I * s:]),
             _vp(self.cell_size[p0 * d:]), _vp(self.dt[p0:]), _vp(self.max_eigenvalue[p0:]), _vp(self.status),
-            kernel_id(kernel), 0, _stream_handle(torch, stream)), "fvb_update")
+            kernel_id(kernel, mode), 0, _stream_handle(torch, stream)), "fvb_update")
 
     def max_eig_prepass(self, stream=None) -> None:
         """Per-patch wave speed of QIn without an update (first-step dt)."""
@@ -325,7 +331,8 @@ def _ensure_pinned(arrays) -> None:
         weakref.finalize(_owner(a), _release)
 
 
-def update_host(batch: PatchBatch, gamma: float, device=None, kernel="auto", chunk_patches: int | None = None):
+def update_host(batch: PatchBatch, gamma: float, device=None, kernel="auto", chunk_patches: int | None = None,
+                mode: str = "exact"):
     """fvb_update_host on the batch's numpy arrays.  Returns the C-ABI code (0 or FVB_ERR_NONPHYSICAL)."""
     torch = _torch()
     dev = torch.device("cuda", torch.cuda.current_device() if device is None else device)
@@ -350,7 +357,7 @@ def update_host(batch: PatchBatch, gamma: float, device=None, kernel="auto", chu
         np.copyto(dts, batch.dt)
         ws, stream = _workspace(torch, dev, need)
         rc = L.fvb_update_host(ctypes.byref(fs), _hp(batch.QIn), _hp(batch.QOut), _hp(cs), _hp(dts), _hp(me),
-                               _vp(ws), ctypes.c_size_t(ws.numel()), chunk, kernel_id(kernel),
+                               _vp(ws), ctypes.c_size_t(ws.numel()), chunk, kernel_id(kernel, mode),
                                ctypes.c_void_p(stream.cuda_stream))
         np.copyto(batch.max_eigenvalue, me)   # fvb_update_host returns after its last D2H
     if rc not in (_lib.FVB_OK, _lib.FVB_ERR_NONPHYSICAL):

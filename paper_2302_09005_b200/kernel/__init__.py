@@ -204,13 +204,17 @@ def raise_first_error(info: np.ndarray, variant, dim: int, p: int) -> None:
 def update_patch_batch(batch: PatchBatch, pde: PdeDefinition, variant: KernelVariant,
                        temporaries: KernelTemporaries | None = None, engine: str = "vectorized", *,
                        device=None, kernel: str = "auto", gamma: float | None = None,
-                       chunk_patches: int | None = None) -> None:
+                       chunk_patches: int | None = None, mode: str = "exact") -> None:
     """Advance every patch of the batch by its own dt (kernel/__init__.py:114-140).
 
     QOut receives the updated interior solution and max_eigenvalue the
     per-patch directional maximum; QIn is read-only.  Extra keyword-only
     arguments select the CUDA device, the kernel ("auto" | "fused" |
-    "generic"), an explicit gamma and the host pipeline chunk size.
+    "generic"), an explicit gamma, the host pipeline chunk size and the
+    arithmetic mode: "exact" (default; bit-identical to the reference) or
+    "fast" (QOut within 1e-12 relative max-norm per unknown -- the north
+    star's parity bar -- with max_eigenvalue still bit-exact; see
+    csrc/fvb_fast3d.cu).  Shapes without a fast kernel run the exact one.
     """
     if batch.n_patches == 0:
         return
@@ -224,7 +228,7 @@ def update_patch_batch(batch: PatchBatch, pde: PdeDefinition, variant: KernelVar
     g = bind_euler(pde, batch.spec.dimensions, gamma)
     from .. import device as _device
 
-    rc = _device.update_host(batch, g, device=device, kernel=kernel, chunk_patches=chunk_patches)
+    rc = _device.update_host(batch, g, device=device, kernel=kernel, chunk_patches=chunk_patches, mode=mode)
     if rc != 0:
         info = _device.locate_host(batch, g, device=device, chunk_patches=chunk_patches)
         raise_first_error(info, variant, batch.spec.dimensions, batch.spec.volumes_per_axis)

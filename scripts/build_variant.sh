@@ -10,14 +10,16 @@ OUT=$ROOT/paper_2302_09005_b200/_variants
 B=$(mktemp -d)
 mkdir -p "$OUT"
 FLAGS="-gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 -fmad=false -Xcompiler -fPIC $*"
-for f in fvb_capi fvb_generic fvb_fused2d fvb_fused2d_warp fvb_fused3d fvb_fused3d_half fvb_fused3d_pair fvb_small3d fvb_halo_tma fvb_mgpu; do
+SRCS=$(sed -n 's/^SRCS = //p' "$SRC/Makefile")
+for cu in $SRCS $EXTRA_SRCS; do
+  f=${cu%.cu}
   /usr/local/cuda/bin/nvcc $FLAGS -Xptxas -v -c "$SRC/$f.cu" -o "$B/$f.o" 2> "$B/$f.log" &
 done
 g++ -O2 -fPIC -std=c++17 -c "$SRC/fvb_io.cpp" -o "$B/fvb_io.o" &
 FAIL=0
 for j in $(jobs -p); do wait $j || FAIL=1; done
 if [ $FAIL = 1 ]; then cat "$B"/*.log | grep -i -B2 -A5 error | head -40; rm -rf "$B"; exit 1; fi
-grep -h -A2 "fused3d_kernelILi0ELi2" "$B/fvb_fused3d.log" | grep -E "registers|spill" || true
+grep -h -A2 "fast3d_kernel" "$B/fvb_fast3d.log" | grep -E "registers|spill" || true
 /usr/local/cuda/bin/nvcc -gencode arch=compute_100a,code=sm_100a -shared -o "$OUT/libfvb200_$NAME.so" "$B"/*.o -ldl
 rm -rf "$B"
 echo "$OUT/libfvb200_$NAME.so"
