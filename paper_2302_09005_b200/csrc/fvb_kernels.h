@@ -35,6 +35,7 @@ bool fvb_fused2d_warp_supported(int p);
 bool fvb_fused2d_use_warp();
 bool fvb_fast3d_supported(int dim, int p, int layout);
 cudaError_t fvb_launch_fast3d16(const FvbArgs& a, cudaStream_t st);
+cudaError_t fvb_launch_fast3d16_rpc(const FvbArgs& a, cudaStream_t st);
 cudaError_t fvb_launch_redo(const FvbArgs& a, cudaStream_t st);
 bool fvb_fused16_supported(int dim, int p, int layout);
 bool fvb_small3d_supported(int dim, int p, int layout);
