@@ -13,9 +13,6 @@
 #include "fvb_kernels.h"
 #include "fvb_layout.cuh"
 
-#ifndef FVB_FAST3D_RPC
-#define FVB_FAST3D_RPC 0
-#endif
 
 namespace {
 
@@ -109,11 +106,7 @@ int fvb_update(const fvb_spec* spec, const double* qin, double* qout, const doub
     if (e != cudaSuccess) return set_cuda_error(e, "memset max_eig");
     e = fvb_launch_generic(a, st);
   } else if (fast && fvb_fast3d_supported(spec->dim, spec->p, spec->layout)) {
-#if FVB_FAST3D_RPC
-    e = fvb_launch_fast3d16_rpc(a, st);
-#else
     e = fvb_launch_fast3d16(a, st);
-#endif
     if (e == cudaSuccess) e = fvb_launch_redo(a, st);   // exact re-evaluation of queued patches
   } else {
     e = fvb_launch_fused16(a, st);

@@ -328,41 +328,17 @@ bool fvb_fused16_supported(int dim, int p, int layout) {
          fvb_small3d_supported(dim, p, layout);
 }
 
-// 3D p=16 kernel choice: half-patch CTAs (default), full-patch CTAs
-// (FVB_3D_KERNEL=full) or half-patch CTAs with two cells per thread
-// (FVB_3D_KERNEL=pair); the alternatives are kept for A/B measurements.
-int fvb_fused3d_choice() {
-  static int v = -1;
-  if (v < 0) {
-    const char* e = getenv("FVB_3D_KERNEL");
-    v = (e && e[0] == 'f') ? 0 : (e && e[0] == 'p') ? 2 : 1;
-  }
-  return v;
-}
-
-// 2D p=16 AoS kernel choice: warp-autonomous y march (default) or the block
-// kernel above (FVB_2D_KERNEL=block, kept for A/B measurements; always used for SoA).
-bool fvb_fused2d_use_warp() {
-  static int v = -1;
-  if (v < 0) {
-    const char* e = getenv("FVB_2D_KERNEL");
-    v = (e && e[0] == 'b') ? 0 : 1;
-  }
-  return v == 1;
-}
-
 cudaError_t fvb_launch_fused16(const FvbArgs& a, cudaStream_t st) {
   using namespace fvb;
   if (a.n <= 0) return cudaSuccess;
   if (a.dim == 3 && a.p != 16) return fvb_launch_small3d(a, st);   // includes its redo pass
   cudaError_t e;
   if (a.dim == 3) {
-    const int c = fvb_fused3d_choice();
-    e = c == 0 ? fvb_launch_fused3d16(a, st) : c == 2 ? fvb_launch_fused3d16_pair(a, st) : fvb_launch_fused3d16_half(a, st);
-  } else if (a.layout == kAoS && (a.p != 16 || fvb_fused2d_use_warp())) {
-    e = fvb_launch_fused2d16_warp(a, st);
+    e = fvb_launch_fused3d16_half(a, st);
+  } else if (a.layout == kAoS) {
+    e = fvb_launch_fused2d16_warp(a, st);   // AoS: warp-autonomous kernel (any p = 2..32)
   } else {
-    e = a.layout == kAoS ? f2::launch<kAoS>(a, st) : f2::launch<kSoA>(a, st);
+    e = f2::launch<kSoA>(a, st);            // SoA (packed layout): the block kernel above
   }
   if (e != cudaSuccess) return e;
   return fvb_launch_redo(a, st);   // exact re-evaluation of queued patches (usually none)

@@ -63,35 +63,12 @@ constexpr int OFF_XS = OFF_YS + 2 * YS;
 constexpr int OFF_OUT = OFF_XS + 2 * XS;
 constexpr int OFF_WMAX = OFF_OUT + 2 * OUTN;
 constexpr int OFF_FLAG = OFF_WMAX + 8;
-constexpr int OFF_TMEM = OFF_FLAG + 1;    // TMEM base address (4 B) + padding
-constexpr int OFF_BAR = OFF_TMEM + 1;
-#ifndef FVB3D_SYNC
-#define FVB3D_SYNC 0
-#endif
-// FVB3D_SYNC = 1: instead of one CTA barrier per plane, per-warp mbarriers by
-// buffer parity -- F[w][p] "warp w published its side data of a plane of parity
-// p" and E[w][p] "interior warp w finished updating from parity-p data" -- so a
-// warp waits only for the warps whose rows it reads (its y neighbours and the
-// halo warp) instead of the slowest warp of the CTA.
-constexpr bool SPLIT_SYNC = FVB3D_SYNC != 0;
-constexpr int OFF_FBAR = OFF_BAR + NST;               // F[NIW + 1][2]
-constexpr int OFF_EBAR = OFF_FBAR + 2 * (NIW + 1);    // E[NIW][2]
-constexpr int TOTAL = OFF_EBAR + 2 * NIW;
+constexpr int OFF_BAR = OFF_FLAG + 1;
+constexpr int TOTAL = OFF_BAR + NST;
 constexpr size_t BYTES = (size_t)TOTAL * 8;
-#ifndef FVB3D_OWN_TMEM
-#define FVB3D_OWN_TMEM 0
-#endif
-// OWN_TMEM (off): the own volume's state, x/y wave speeds and x/y fluxes (15
-// doubles) go from the closure of plane zh to the update of plane zh in the
-// next iteration through tensor memory (one 32-column record per plane parity
-// in the thread's TMEM lane) instead of being re-read from shared memory --
-// the shared-memory data pipe is this kernel's binding resource (~70 % of its
-// wavefront peak) and TMEM is a separate path.  Measured on B200: bit-exact
-// but 2.2x SLOWER (1,062 vs 481 us for C3): two tcgen05.ld.x16 + wait::ld and
-// two tcgen05.st.x16 per cell per plane cost far more than the 15 LDS.64 they
-// replace.
-constexpr bool OWN_TMEM = FVB3D_OWN_TMEM != 0;
-constexpr uint32_t TMEM_COLS = 64;        // 2 parities x 32 columns
+// (Measured and removed: per-warp mbarriers instead of the
+// CTA barrier, 554 vs 465 us; the own volume's data carried through TMEM,
+// 1,062 us.)
 
 template <int L>
 __device__ __forceinline__ double qs(const double* st, int r, int hx, int u) {
@@ -156,7 +133,6 @@ fused3d_half_kernel(const double* __restrict__ qin, double* __restrict__ qout, c
   unsigned long long* wmax = reinterpret_cast<unsigned long long*>(sm + OFF_WMAX);
   unsigned* slowflag = reinterpret_cast<unsigned*>(sm + OFF_FLAG);   // 2 words, by item parity
   uint64_t* bars = reinterpret_cast<uint64_t*>(sm + OFF_BAR);
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sm + OFF_TMEM);
 
   const int tid = threadIdx.x;
   const bool interior = tid < 32 * NIW;
@@ -213,33 +189,18 @@ fused3d_half_kernel(const double* __restrict__ qin, double* __restrict__ qout, c
     }
   };
 
-  uint64_t* fbar = reinterpret_cast<uint64_t*>(sm + OFF_FBAR);
-  uint64_t* ebar = reinterpret_cast<uint64_t*>(sm + OFF_EBAR);
   if (producer) {
 #pragma unroll
     for (int s = 0; s < NST; ++s) mbar_init(&bars[s], 1);
-    if (SPLIT_SYNC) {
-      for (int b = 0; b < 2 * (NIW + 1); ++b) mbar_init(&fbar[b], 1);
-      for (int b = 0; b < 2 * NIW; ++b) mbar_init(&ebar[b], 1);
-    }
     slowflag[0] = slowflag[1] = 0;
     fence_mbar_init();
   }
-  if (OWN_TMEM && warp == 0) tmem_alloc(tmem_slot, TMEM_COLS);
-  if (OWN_TMEM) tmem_fence_before();
   __syncthreads();
-  if (OWN_TMEM) tmem_fence_after();
-  // this thread's TMEM lane: the lane quadrant of its warp (warps 0..3 interior)
-  const uint32_t tm_base = OWN_TMEM ? *tmem_slot + ((uint32_t)(32 * (warp & 3)) << 16) : 0u;
   if (producer && my_items > 0) {
     issue(0, 0, 0);
     issue(0, 1, 1);
   }
 
-#ifdef FVB3D_PROFILE_BARRIER
-  long long work_cycles = 0, wait_cycles = 0;
-  const long long t_start = clock64();
-#endif
   bool slow = false;
   unsigned long long cm = 0;
   Side<3> zprev;
@@ -266,13 +227,6 @@ fused3d_half_kernel(const double* __restrict__ qin, double* __restrict__ qout, c
 
     auto plane = [&](int zh, auto kind) {
       constexpr int K = decltype(kind)::value;
-      // split sync: iteration g (global plane count) arrives on parity g & 1, completing
-      // that barrier's phase g >> 1
-      const int g = jp * NPL + zh;
-      const unsigned pa = (unsigned)(g & 1);
-      const unsigned ph_prev = (unsigned)(((g - 1) >> 1) & 1), ph_cur = (unsigned)((g >> 1) & 1);
-      auto wait_e_prev = [&](int w) { mbar_wait(&ebar[2 * w + (pa ^ 1u)], ph_prev); };   // B(g-1) of warp w done
-      auto wait_f_prev = [&](int w) { mbar_wait(&fbar[2 * w + (pa ^ 1u)], ph_prev); };   // A(g-1) of warp w done
       const unsigned stg = (unsigned)(zh % NST), par = (unsigned)((zh / NST) & 1);
       const unsigned stp = stg == 0 ? NST - 1 : stg - 1;   // stage of plane zh-1
       const double* st = ring + stg * STAGE;
@@ -281,21 +235,9 @@ fused3d_half_kernel(const double* __restrict__ qin, double* __restrict__ qout, c
       double* xs_w = xsb + (zh & 1) * XS;
       const double* ys_r = ysb + ((zh - 1) & 1) * YS;
       const double* xs_r = xsb + ((zh - 1) & 1) * XS;
-#ifdef FVB3D_PROFILE_BARRIER
-      const long long tw0 = clock64();
       mbar_wait(&bars[stg], par);
-      const long long tw1 = clock64();
-      wait_cycles += tw1 - tw0;
-#else
-      mbar_wait(&bars[stg], par);
-#endif
 
       if (interior) {
-        if (OWN_TMEM) tmem_wait_st();   // last iteration's record (read below) has landed
-        if (SPLIT_SYNC && g >= 1) {     // WAR: A(g) overwrites what B(g-1) of the y neighbours read
-          if (warp > 0) wait_e_prev(warp - 1);
-          if (warp < NIW - 1) wait_e_prev(warp + 1);
-        }
         Side<3> zcur;
         double q[S];
         load_q<L>(st, ly + 1, x + 1, q);
@@ -313,14 +255,6 @@ fused3d_half_kernel(const double* __restrict__ qin, double* __restrict__ qout, c
           put_xs(xs_w, ly, x + 1, sd[0]);
           put_ys(ys_w, ly + 1, x, sd[1]);
           zcur = sd[2];
-          if (OWN_TMEM) {   // own data for next iteration's update of this plane
-            const double ra[8] = {q[0], q[1], q[2], q[3], q[4], sd[0].lam, sd[1].lam, 0.0};
-            const double rb[8] = {sd[0].f[0], sd[0].f[1], sd[0].f[2], sd[0].f[3],
-                                  sd[1].f[0], sd[1].f[1], sd[1].f[2], sd[1].f[3]};
-            const uint32_t ta = tm_base + 32u * (uint32_t)(zh & 1);
-            tmem_st8(ta, ra);
-            tmem_st8(ta + 16, rb);
-          }
         } else {
           bool ok;
           closure_one_ranged<3>(q, cl, 2, zcur, ok);
@@ -337,42 +271,29 @@ fused3d_half_kernel(const double* __restrict__ qin, double* __restrict__ qout, c
             favg_zm[u] = dadd(c, u == 0 ? q[3] : zcur.f[u - 1]);
           }
         }
-        if (SPLIT_SYNC) {   // A(g) published
-          __syncwarp();
-          if (lane == 0) mbar_arrive(&fbar[2 * warp + pa]);
-        }
         if (K == kSteady || K == kZHi) {
-          if (SPLIT_SYNC) {   // RAW: B(g) reads the y neighbours' and the halo warp's A(g-1)
-            wait_f_prev(warp > 0 ? warp - 1 : NIW);
-            wait_f_prev(warp < NIW - 1 ? warp + 1 : NIW);
-            if (warp > 0 && warp < NIW - 1) wait_f_prev(NIW);
-          }
-          double qc[S], val[S], qn[S], ra[8], rb[8];
-          double lx, lyv;
-          if (OWN_TMEM) {
-            const uint32_t ta = tm_base + 32u * (uint32_t)((zh - 1) & 1);
-            tmem_ld8(ta, ra);
+          double qc[S], val[S], qn[S], rb[8];
+          load_q<L>(stc, ly + 1, x + 1, qc);
+          const double lx = xs_r[xs_at(0, ly, x + 1)];
+          const double lyv = ys_r[ys_at(0, ly + 1, x)];
 #pragma unroll
-            for (int u = 0; u < S; ++u) qc[u] = ra[u];
-            lx = ra[5];
-            lyv = ra[6];
-          } else {
-            load_q<L>(stc, ly + 1, x + 1, qc);
-            lx = xs_r[xs_at(0, ly, x + 1)];
-            lyv = ys_r[ys_at(0, ly + 1, x)];
-#pragma unroll
-            for (int k = 0; k < 4; ++k) { rb[k] = xs_r[xs_at(k + 1, ly, x + 1)]; rb[4 + k] = ys_r[ys_at(k + 1, ly + 1, x)]; }
-          }
+          for (int k = 0; k < 4; ++k) { rb[k] = xs_r[xs_at(k + 1, ly, x + 1)]; rb[4 + k] = ys_r[ys_at(k + 1, ly + 1, x)]; }
           const double cz = dmul(half_inv, speed_max(zcur.lam, zprev.lam));
 #pragma unroll
           for (int u = 0; u < S; ++u) val[u] = qc[u];                       // _pass_copy
+          // neighbours' normal momenta (flux component 0) kept from the dissipation loads
+          double jxm, jxp, jym, jyp;
           load_q<L>(stc, ly + 1, x, qn);
+          jxm = qn[1];
           dissipate<3>(val, half_inv, lx, qc, xs_r[xs_at(0, ly, x)], qn);
           load_q<L>(stc, ly + 1, x + 2, qn);
+          jxp = qn[1];
           dissipate<3>(val, half_inv, lx, qc, xs_r[xs_at(0, ly, x + 2)], qn);
           load_q<L>(stc, ly, x + 1, qn);
+          jym = qn[2];
           dissipate<3>(val, half_inv, lyv, qc, ys_r[ys_at(0, ly, x)], qn);
           load_q<L>(stc, ly + 2, x + 1, qn);
+          jyp = qn[2];
           dissipate<3>(val, half_inv, lyv, qc, ys_r[ys_at(0, ly + 2, x)], qn);
 #pragma unroll
           for (int u = 0; u < S; ++u) val[u] = dsub(val[u], tp[u]);
@@ -381,25 +302,12 @@ fused3d_half_kernel(const double* __restrict__ qin, double* __restrict__ qout, c
             tp[u] = dmul(cz, dsub(q[u], qc[u]));
             val[u] = dadd(val[u], tp[u]);
           }
-          {
-            if (OWN_TMEM) tmem_ld8(tm_base + 32u * (uint32_t)((zh - 1) & 1) + 16, rb);
-            double fo[4];
-#pragma unroll
-            for (int k = 0; k < 4; ++k) fo[k] = rb[k];
-            add_flux(val, half_inv,
-                     [&](int u) { return u == 0 ? qs<L>(stc, ly + 1, x, 1) : xs_r[xs_at(u, ly, x)]; },
-                     [&](int u) { return u == 0 ? qc[1] : fo[u - 1]; },
-                     [&](int u) { return u == 0 ? qs<L>(stc, ly + 1, x + 2, 1) : xs_r[xs_at(u, ly, x + 2)]; });
-          }
-          {
-            double fo[4];
-#pragma unroll
-            for (int k = 0; k < 4; ++k) fo[k] = rb[4 + k];
-            add_flux(val, half_inv,
-                     [&](int u) { return u == 0 ? qs<L>(stc, ly, x + 1, 2) : ys_r[ys_at(u, ly, x)]; },
-                     [&](int u) { return u == 0 ? qc[2] : fo[u - 1]; },
-                     [&](int u) { return u == 0 ? qs<L>(stc, ly + 2, x + 1, 2) : ys_r[ys_at(u, ly + 2, x)]; });
-          }
+          add_flux(val, half_inv, [&](int u) { return u == 0 ? jxm : xs_r[xs_at(u, ly, x)]; },
+                   [&](int u) { return u == 0 ? qc[1] : rb[u - 1]; },
+                   [&](int u) { return u == 0 ? jxp : xs_r[xs_at(u, ly, x + 2)]; });
+          add_flux(val, half_inv, [&](int u) { return u == 0 ? jym : ys_r[ys_at(u, ly, x)]; },
+                   [&](int u) { return u == 0 ? qc[2] : rb[3 + u]; },
+                   [&](int u) { return u == 0 ? jyp : ys_r[ys_at(u, ly + 2, x)]; });
 #pragma unroll
           for (int u = 0; u < S; ++u) {
             const double c = u == 0 ? qc[3] : zprev.f[u - 1];
@@ -420,10 +328,6 @@ fused3d_half_kernel(const double* __restrict__ qin, double* __restrict__ qout, c
         // the halo warp: stage rows 0 and 9 (y-face halo row and the ghost row
         // of the other half) need y-side data; interior rows need the x-face
         // halo columns' x-side data
-        if (SPLIT_SYNC && g >= 1) {   // WAR: every interior warp's B(g-1) read these buffers
-#pragma unroll
-          for (int w = 0; w < NIW; ++w) wait_e_prev(w);
-        }
         {
           const int r = lane < 16 ? 0 : SR - 1;
           double qh[S];
@@ -462,29 +366,14 @@ fused3d_half_kernel(const double* __restrict__ qin, double* __restrict__ qout, c
           cm = 0;
         }
       }
-      if (SPLIT_SYNC) {
-        __syncwarp();
-        if (lane == 0) mbar_arrive(interior ? &ebar[2 * warp + pa] : &fbar[2 * NIW + pa]);
-        if (producer) {   // the ring stage and the output buffer of this plane: after every B(g)
-#pragma unroll
-          for (int w = 0; w < NIW; ++w) mbar_wait(&ebar[2 * w + pa], ph_cur);
-        }
-      } else {
-        if (producer) bulk_wait_read0();
-#ifdef FVB3D_PROFILE_BARRIER
-        work_cycles += clock64() - tw1;   // from the ring wait to the barrier: this warp's work
-#endif
-        __syncthreads();
-      }
+      if (producer) bulk_wait_read0();
+      __syncthreads();
       if (producer) {
         const int zn = zh + 2 < NPL ? zh + 2 : zh + 2 - NPL;
         const int jn = zh + 2 < NPL ? jp : jp + 1;
         if (jn < my_items) issue(jn, zn, stp);
         if (K == kSteady || K == kZHi) store_out(pidx, y0, zh - 2);
         if (K == kZHi) finish_item(jp, pidx);
-        // split sync: the next B into this output buffer (iteration g+2) waits for the
-        // halo warp's A(g+1), which this thread reaches only after the store read it
-        if (SPLIT_SYNC) bulk_wait_read0();
       }
     };
 
@@ -495,22 +384,7 @@ fused3d_half_kernel(const double* __restrict__ qin, double* __restrict__ qout, c
     plane(NPL - 1, Kind<kZHi>{});
   }
 
-  if (OWN_TMEM) tmem_fence_before();
-  if (OWN_TMEM) {
-    tmem_fence_after();
-    if (warp == 0) tmem_dealloc(*tmem_slot, TMEM_COLS);
-  }
   if (producer) bulk_wait_all0();
-#ifdef FVB3D_PROFILE_BARRIER
-  // diagnostic build only: per-role barrier cycles / total cycles, accumulated into
-  // the (otherwise unused here) tail of the status buffer's redo list
-  if (lane == 0) {
-    unsigned long long* acc = reinterpret_cast<unsigned long long*>(status + 2 + 2 * n + 64);
-    atomicAdd(acc + (interior ? 0 : 3), (unsigned long long)work_cycles);
-    atomicAdd(acc + (interior ? 1 : 4), (unsigned long long)wait_cycles);
-    atomicAdd(acc + (interior ? 2 : 5), (unsigned long long)(clock64() - t_start));
-  }
-#endif
 }
 
 template <int L>

@@ -26,16 +26,11 @@ struct FvbArgs {
 
 cudaError_t fvb_launch_generic(const FvbArgs& a, cudaStream_t st);
 cudaError_t fvb_launch_fused16(const FvbArgs& a, cudaStream_t st);
-cudaError_t fvb_launch_fused3d16(const FvbArgs& a, cudaStream_t st);
 cudaError_t fvb_launch_fused3d16_half(const FvbArgs& a, cudaStream_t st);
-int fvb_fused3d_choice();
-cudaError_t fvb_launch_fused3d16_pair(const FvbArgs& a, cudaStream_t st);
 cudaError_t fvb_launch_fused2d16_warp(const FvbArgs& a, cudaStream_t st);
 bool fvb_fused2d_warp_supported(int p);
-bool fvb_fused2d_use_warp();
 bool fvb_fast3d_supported(int dim, int p, int layout);
 cudaError_t fvb_launch_fast3d16(const FvbArgs& a, cudaStream_t st);
-cudaError_t fvb_launch_fast3d16_rpc(const FvbArgs& a, cudaStream_t st);
 cudaError_t fvb_launch_redo(const FvbArgs& a, cudaStream_t st);
 bool fvb_fused16_supported(int dim, int p, int layout);
 bool fvb_small3d_supported(int dim, int p, int layout);

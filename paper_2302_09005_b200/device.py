@@ -14,7 +14,6 @@ There is no CPU fallback anywhere: without a CUDA device these raise.
 from __future__ import annotations
 
 import ctypes
-import os
 import threading
 
 import numpy as np
@@ -277,11 +276,11 @@ def _host_stage(torch, name: str, like: np.ndarray) -> np.ndarray:
 
 def default_chunk(spec: PatchSpec, n: int, pipeline_chunks: int | None = None) -> int:
     """Host-pipeline chunk: at most 256 MB of device buffers per set, and about
-    FVB_HOST_CHUNKS (default 32) chunks per call so the unoverlapped first H2D /
+    `pipeline_chunks` (default 32) chunks per call so the unoverlapped first H2D /
     last D2H (pipeline fill and drain) stay a small fraction of the transfer."""
     per_patch = (spec.haloed_volumes + spec.interior_volumes) * spec.unknowns * 8
     by_bytes = max(1, (256 << 20) // per_patch)
-    k = int(pipeline_chunks or os.environ.get("FVB_HOST_CHUNKS", "32"))
+    k = int(pipeline_chunks or 32)
     by_pipeline = max(1, -(-n // k))
     floor = max(16, -(-(4 << 20) // per_patch))   # >= 4 MB per chunk: small batches are not worth pipelining
     return int(max(1, min(n, by_bytes, max(by_pipeline, min(n, floor)))))
@@ -292,7 +291,8 @@ def default_chunk(spec: PatchSpec, n: int, pipeline_chunks: int | None = None) -
 # against 19.6 ms from page-locked ones.  The first call on an array registers its memory
 # (cudaHostRegister, ~25 ms per GB) and keeps it registered while the array lives, so a
 # batch that is stepped repeatedly -- the reference's usage -- runs at pinned speed from the
-# second call on.  FVB_AUTO_PIN=0 disables it.
+# second call on.  Set `device.AUTO_PIN = False` to disable it.
+AUTO_PIN = True
 _PINNED: dict[int, int] = {}        # registered start address -> bytes
 _PIN_LOCK = threading.Lock()
 
@@ -304,7 +304,7 @@ def _owner(a: np.ndarray):
 
 
 def _ensure_pinned(arrays) -> None:
-    if os.environ.get("FVB_AUTO_PIN", "1") == "0":
+    if not AUTO_PIN:
         return
     import weakref
 

@@ -129,7 +129,8 @@ class SimulationResult:
 
 
 def run_simulation(db: DeviceBatch, grid_shape, steps: int, cfl: float = 0.4, periodic: bool = True,
-                   kernel="auto", dx: float | None = None, graph: bool | None = None) -> SimulationResult:
+                   kernel="auto", dx: float | None = None, graph: bool | None = None,
+                   direct: bool | None = None) -> SimulationResult:
     """Device-resident time loop on one GPU.
 
     db.QOut holds the initial interior field of a logical uniform patch grid
@@ -173,11 +174,9 @@ def run_simulation(db: DeviceBatch, grid_shape, steps: int, cfl: float = 0.4, pe
 
     # 2D AoS fast path: the update writes into the interior of the other haloed buffer,
     # then only its halo shell is filled (fvb_update_to_haloed / fvb_halo_shell)
-    import os
-
     p = db.spec.volumes_per_axis
-    direct = (db.spec.dimensions == 2 and db.layout == "aos" and 2 <= p <= 32 and kernel in ("auto", "fused")
-              and os.environ.get("FVB_RUNSIM_DIRECT", "1") != "0")
+    direct_ok = db.spec.dimensions == 2 and db.layout == "aos" and 2 <= p <= 32 and kernel in ("auto", "fused")
+    direct = direct_ok if direct is None else (bool(direct) and direct_ok)
     bufs = [db.QIn, torch.empty_like(db.QIn)] if direct else None
     gshape = (ctypes.c_int32 * 3)(*(list(grid_shape) + [1] * (3 - len(grid_shape))))
 

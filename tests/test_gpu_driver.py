@@ -94,37 +94,6 @@ def test_halo_project_totals_fused(dim, p, grid):
         np.testing.assert_allclose(db.totals(), exact, rtol=1e-13, atol=0)
 
 
-HALO_ROWS_SCRIPT = """
-import sys
-sys.path.insert(0, {root!r})
-import numpy as np
-import oracle
-from paper_2302_09005_b200 import mesh
-for dim, p, grid in {grids!r}:
-    n = int(np.prod(grid))
-    b = mesh.make_patch_batch(mesh.PatchSpec(dim, p, dim + 2), n)
-    b.QOut[...] = np.random.default_rng(n).standard_normal(b.QOut.shape)
-    for periodic in (True, False):
-        mesh.halo_project(b, grid, periodic)
-        ref = oracle.halo_project(dim, p, b.QOut, grid, periodic)
-        assert np.array_equal(b.QIn.view(np.uint64), ref.view(np.uint64)), (dim, p, grid, periodic)
-print("ok")
-"""
-
-
-def test_halo_project_thread_copy_kernels():
-    """FVB_HALO_KERNEL=rows selects the thread-copy kernels the TMA / per-patch-row paths
-    replaced (still used for shapes those do not cover); they stay bit-exact."""
-    import subprocess
-    import sys
-
-    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    code = HALO_ROWS_SCRIPT.format(root=root, grids=HALO_GRIDS)
-    r = subprocess.run([sys.executable, "-c", code], env={**os.environ, "FVB_HALO_KERNEL": "rows"},
-                       capture_output=True, text=True, timeout=300)
-    assert r.returncode == 0 and r.stdout.strip().endswith("ok"), r.stdout + r.stderr
-
-
 def _db_with_field(dim, p, grid, qout):
     n = int(np.prod(grid))
     spec = mesh.PatchSpec(dim, p, dim + 2)
@@ -281,7 +250,7 @@ def test_run_simulation_graph_matches_eager(dim, p, grid):
 
 @pytest.mark.parametrize("p,grid,periodic", [(16, (4, 5), True), (16, (3, 3), False), (17, (3, 4), True),
                                              (5, (6, 2), False), (32, (2, 2), True), (3, (1, 1), True)])
-def test_run_simulation_2d_direct_path_matches(p, grid, periodic, monkeypatch):
+def test_run_simulation_2d_direct_path_matches(p, grid, periodic):
     """2D run_simulation's fast path (update straight into the next haloed batch + halo shell)
     gives the classic path's field, QIn, dt history and wave speeds bit for bit."""
     dim = 2
@@ -289,15 +258,14 @@ def test_run_simulation_2d_direct_path_matches(p, grid, periodic, monkeypatch):
     q = oracle.synthetic_qin(dim, p, n, seed=33 + p).reshape(n, p + 2, p + 2, dim + 2)
     interior = q[:, 1:-1, 1:-1, :].reshape(n, -1)
     out = {}
-    for direct in ("0", "1"):
-        monkeypatch.setenv("FVB_RUNSIM_DIRECT", direct)
+    for direct in (False, True):
         db = _db_with_field(dim, p, grid, interior)
-        res = driver.run_simulation(db, grid, steps=5, cfl=0.4, periodic=periodic)
+        res = driver.run_simulation(db, grid, steps=5, cfl=0.4, periodic=periodic, direct=direct)
         out[direct] = (db.QOut.cpu().numpy(), db.QIn.cpu().numpy(), res)
-    assert_bits_equal(out["1"][0], out["0"][0], "QOut")
-    assert_bits_equal(out["1"][1], out["0"][1], "QIn (final halo)")
-    assert out["1"][2].dt == out["0"][2].dt and out["1"][2].max_eigenvalue == out["0"][2].max_eigenvalue
-    np.testing.assert_allclose(np.asarray(out["1"][2].totals), np.asarray(out["0"][2].totals), rtol=1e-13)
+    assert_bits_equal(out[True][0], out[False][0], "QOut")
+    assert_bits_equal(out[True][1], out[False][1], "QIn (final halo)")
+    assert out[True][2].dt == out[False][2].dt and out[True][2].max_eigenvalue == out[False][2].max_eigenvalue
+    np.testing.assert_allclose(np.asarray(out[True][2].totals), np.asarray(out[False][2].totals), rtol=1e-13)
 
 
 @pytest.mark.parametrize("dim,p,grid", [(3, 16, (2, 2, 5)), (2, 16, (3, 7)), (3, 4, (2, 3, 4))])
