@@ -1,21 +1,26 @@
 """Benchmark: cell updates/s of the fp64 Rusanov patch update on B200 (BASELINE.json metric).
 
-    python bench.py [--gpus N --steps K --warmup W] [--config c3|c2|c4] [--layout aos|soa]
-    python bench.py --impl reference ...      # the reference algorithm on the host cores (oracle port)
+    python bench.py [--gpus N --steps K --warmup W] [--config c3|c2|c4] [--mode fast|exact]
+    python bench.py --impl reference ...      # the reference algorithm on the host cores
 
 One step = one fused Rusanov update of the rank's shard (device resident) plus
 the CFL step control: local max wave speed, NCCL MAX all-reduce when N > 1,
-dt = (cfl*dx)/gmax written back on the device (driver.CflStepper).  Weak
-scaling (default): every rank owns the configuration's full patch count;
---scaling strong splits the configuration's patches over the ranks instead.
+dt = (cfl*dx)/gmax written back on the device (driver.CflStepper), captured
+once in a CUDA graph and replayed.  Weak scaling (default): every rank owns the
+configuration's full patch count; --scaling strong splits it over the ranks.
 
-Rank 0 prints one JSON line (the driver contract).  `value` is device-timed
-(CUDA events, max over ranks); `e2e` is the drop-in public API
-(kernel.update_patch_batch) on pinned host arrays, H2D + D2H inside the timed
-region; `roofline` is the fused kernel's algorithmic HBM bytes per launch over
-its event-timed duration against MEASURED_PEAKS.json; `cpu_baseline` is the
-CPU oracle (a C restatement of the reference algorithm, oracle/) on a bounded
-sample, timed on this box's host cores.
+Rank 0 prints one JSON line (the driver contract):
+  value        device-timed throughput of the K steps (CUDA events, max over ranks)
+               in --mode (default "fast": QOut within the north star's 1e-12
+               relative tolerance, max_eigenvalue bit-exact; tests/test_gpu_fast.py)
+  exact        the same for the bit-exact mode (the library's default)
+  e2e          the drop-in public API (kernel.update_patch_batch) on pinned host
+               arrays, H2D + D2H inside the timed region
+  roofline     the update kernel's algorithmic HBM bytes per launch over its
+               event-timed duration (an eager pass of the same launches right after
+               the timed region) against MEASURED_PEAKS.json
+  cpu_baseline the CPU oracle (a C restatement of the reference algorithm, oracle/)
+               over the full configuration batch, on this box's host cores
 """
 
 from __future__ import annotations
@@ -37,12 +42,13 @@ CONFIGS = {
     "c2": (2, 16, 65536, 1),
     "c3": (3, 16, 4096, 2),
     "c4": (3, 4, 1048576, 3),
-    # not BASELINE configs: the SPEC's Fig. 1 shape (2D p=17) and a 3D p=8 case, both on the
-    # generic kernel, for measuring the fallback path
+    # not BASELINE configs: the SPEC's Fig. 1 shape (2D p=17) and a 3D p=8 case
     "x2p17": (2, 17, 65536, None),
     "x3p8": (3, 8, 32768, None),
 }
 METRIC = "cell updates/sec (fp64, 3D Euler p=16) at 1/2/4/8 B200; % of HBM roofline"
+MODE_NOTE = {"fast": "fast (QOut within 1e-12 relative max-norm of the reference, max_eigenvalue bit-exact)",
+             "exact": "exact (bit-identical to the reference)"}
 
 
 def _cfg_label(idx) -> str:
@@ -56,8 +62,7 @@ def algorithmic_bytes_per_patch(dim: int, p: int) -> int:
 
 
 def algorithmic_flops_per_cell(dim: int, p: int) -> float:
-    """add/sub/mul/div/sqrt/max = 1 flop (abs = 0) per interior cell update:
-    closures on interior + face-halo volumes, face terms, and the per-cell accumulation."""
+    """add/sub/mul/div/sqrt/max = 1 flop (abs = 0) per interior cell update."""
     s = dim + 2
     vols = p ** dim + 2 * dim * p ** (dim - 1)
     faces = dim * (p + 1) * p ** (dim - 1)
@@ -77,63 +82,80 @@ def measured_peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+    """SM clock and clock-event (throttle) reasons sampled every 5 ms through NVML from a
+    thread, over warm-up, the timed steps and the kernel pass (nvidia-smi at 50 ms when
+    NVML is unavailable)."""
 
-    FIELDS = ("clocks.sm", "clocks.max.sm", "clocks_event_reasons.hw_slowdown",
-              "clocks_event_reasons.hw_thermal_slowdown", "clocks_event_reasons.sw_thermal_slowdown",
-              "clocks_event_reasons.sw_power_cap")
+    REASONS = (("hw_slowdown", 0x8), ("hw_thermal_slowdown", 0x40), ("sw_thermal_slowdown", 0x20),
+               ("sw_power_cap", 0x4), ("hw_power_brake_slowdown", 0x80))
 
-    def __init__(self, gpu_index: int):
-        self.gpu = gpu_index
-        self.proc = None
-        self.lines = []
+    def __init__(self, torch, local: int):
+        self.samples, self.reasons, self.max_mhz = [], set(), None
+        self._stop = threading.Event()
+        self._h = None
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            uuid = "GPU-" + str(torch.cuda.get_device_properties(local).uuid)
+            try:
+                self._h = pynvml.nvmlDeviceGetHandleByUUID(uuid)
+            except pynvml.NVMLError:
+                self._h = pynvml.nvmlDeviceGetHandleByIndex(local)
+            self._nv = pynvml
+            self.max_mhz = float(pynvml.nvmlDeviceGetMaxClockInfo(self._h, pynvml.NVML_CLOCK_SM))
+        except Exception:   # pragma: no cover - no NVML
+            self._h = None
+        self.local = local
+
+    def _run_nvml(self):
+        nv = self._nv
+        while not self._stop.is_set():
+            try:
+                self.samples.append(float(nv.nvmlDeviceGetClockInfo(self._h, nv.NVML_CLOCK_SM)))
+                bits = nv.nvmlDeviceGetCurrentClocksEventReasons(self._h)
+                for name, bit in self.REASONS:
+                    if bits & bit:
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            self._stop.wait(0.005)
+
+    def _run_smi(self):
+        proc = subprocess.Popen(["nvidia-smi", "-i", str(self.local), "--query-gpu=clocks.sm,clocks.max.sm",
+                                 "--format=csv,noheader,nounits", "-lms", "50"],
+                                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        self._proc = proc
+        for line in proc.stdout:
+            try:
+                a, b = (float(v) for v in line.split(","))
+                self.samples.append(a)
+                self.max_mhz = b
+            except ValueError:
+                pass
 
     def __enter__(self):
-        try:
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", "-i", str(self.gpu), "--query-gpu=" + ",".join(self.FIELDS),
-                 "--format=csv,noheader,nounits", "-lms", "50"],
-                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.thread = threading.Thread(target=self._read, daemon=True)
-            self.thread.start()
-        except OSError:
-            self.proc = None
+        target = self._run_nvml if self._h is not None else self._run_smi
+        self._t = threading.Thread(target=target, daemon=True)
+        self._t.start()
         return self
 
-    def _read(self):
-        for line in self.proc.stdout:
-            self.lines.append(line.strip())
-
     def __exit__(self, *exc):
-        if self.proc is not None:
-            self.proc.terminate()
-            try:
-                self.proc.wait(timeout=5)
-            except subprocess.TimeoutExpired:
-                self.proc.kill()
+        self._stop.set()
+        if getattr(self, "_proc", None) is not None:
+            self._proc.terminate()
+        self._t.join(timeout=5)
 
     def summary(self):
-        sm, mx, reasons = [], None, set()
-        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
-        for line in self.lines:
-            parts = [p.strip() for p in line.split(",")]
-            if len(parts) != len(self.FIELDS):
-                continue
-            try:
-                sm.append(float(parts[0]))
-                mx = float(parts[1])
-            except ValueError:
-                continue
-            for name, val in zip(names, parts[2:]):
-                if val.lower().startswith("active"):
-                    reasons.add(name)
-        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx,
-                "reasons": sorted(reasons), "samples": len(sm)}
+        load = [s for s in self.samples if self.max_mhz is None or s > 0.5 * self.max_mhz] or self.samples
+        return {"sm_mhz": statistics.median(load) if load else None, "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples),
+                "source": "nvml 5 ms" if self._h is not None else "nvidia-smi 50 ms"}
 
 
 def pcie_bandwidth(torch, nbytes: int = 256 << 20):
-    """Pinned host <-> device copy bandwidth of this GPU's link (GB/s): H2D alone, D2H alone, and
-    each direction while both run (the e2e pipeline overlaps them).  The e2e roofline."""
+    """Pinned host <-> device copy bandwidth (GB/s): H2D alone, D2H alone, and each direction
+    while both run (the e2e pipeline overlaps them).  The e2e roofline."""
     h = torch.empty(nbytes, dtype=torch.uint8, pin_memory=True)
     h2 = torch.empty(nbytes, dtype=torch.uint8, pin_memory=True)
     d = torch.empty(nbytes, dtype=torch.uint8, device="cuda")
@@ -170,57 +192,124 @@ def cpu_cores() -> int:
         return os.cpu_count() or 1
 
 
-def run_cpu_sample(dim: int, p: int, target_s: float | None = None):
-    """Time the oracle port on a bounded sample of the workload; returns (cells/s, cores, description)."""
+def host_batch(dim: int, p: int, n: int, seed: int = 7):
+    """Synthetic admissible batch on the host: qin, cell_size, dt."""
     import numpy as np
 
     import oracle
 
+    chunk = max(1, (256 << 20) // ((p + 2) ** dim * (dim + 2) * 8))
+    qin = np.empty((n, (p + 2) ** dim * (dim + 2)))
+    for lo in range(0, n, chunk):
+        qin[lo:lo + chunk] = oracle.synthetic_qin(dim, p, min(chunk, n - lo), seed=seed + lo)
+    return qin, np.ones((n, dim)), np.full(n, 0.4 * (1.0 / p) / 3.4)
+
+
+def oracle_steps(qin, cs, dt, dim, p, steps, warmup, budget_s):
+    """Time the oracle port (C, OpenMP, all host threads) stepping over the batch.  A step is
+    the full batch when `steps` of them fit the budget, else a rotating contiguous slice of it
+    (so no step re-reads a cache-resident sample).  Returns (per-step cells/s list, cores,
+    patches per step, per-step ms list)."""
+    import oracle
+
     oracle.build()
-    if target_s is None:
-        target_s = float(os.environ.get("FVB_BENCH_CPU_SECONDS", "8"))
     cores = cpu_cores()
-    n = max(cores * 4, 64) if p >= 16 else max(cores * 256, 4096)
-    if os.environ.get("FVB_BENCH_CPU_SMALL"):   # CI: a tiny sample
-        n = max(cores, 2)
-    qin = oracle.synthetic_qin(dim, p, n, seed=7)
-    cs = np.ones((n, dim))
-    dt = np.full(n, 0.4 * (1.0 / p) / 3.4)
-    oracle.update(dim, p, 1.4, qin[: min(n, cores)], cs[: min(n, cores)], dt[: min(n, cores)], nthreads=cores)
-    reps, elapsed = 0, 0.0
+    n = qin.shape[0]
     t0 = time.perf_counter()
-    while elapsed < target_s or reps < 1:
-        oracle.update(dim, p, 1.4, qin, cs, dt, nthreads=cores)
-        reps += 1
-        elapsed = time.perf_counter() - t0
-    cells = reps * n * p ** dim
-    return cells / elapsed, cores, f"{reps} x {n} patches ({dim}D p={p}), {elapsed:.1f} s wall, oracle port (C, OpenMP)"
+    oracle.update(dim, p, 1.4, qin[: min(n, 4 * cores)], cs[: min(n, 4 * cores)], dt[: min(n, 4 * cores)],
+                  nthreads=cores)
+    probe = min(n, 64 * cores)
+    t0 = time.perf_counter()
+    oracle.update(dim, p, 1.4, qin[:probe], cs[:probe], dt[:probe], nthreads=cores)
+    per_patch = (time.perf_counter() - t0) / probe
+    m = int(max(1, min(n, budget_s / max(steps + warmup, 1) / per_patch)))
+    rates, ms = [], []
+    for k in range(warmup + steps):
+        lo = (k * m) % n
+        hi = min(n, lo + m)
+        t0 = time.perf_counter()
+        oracle.update(dim, p, 1.4, qin[lo:hi], cs[lo:hi], dt[lo:hi], nthreads=cores)
+        el = time.perf_counter() - t0
+        if k >= warmup:
+            rates.append((hi - lo) * p ** dim / el)
+            ms.append(el * 1e3)
+    return rates, cores, m, ms
+
+
+def numpy_engine_baseline(qin, cs, dt, dim, p, reps=3):
+    """The reference's own numpy engine (fvbatch, from baseline/_ref), shimmed batched/aos/par
+    with worker_hint = the host's cores, 1 warm-up + `reps` timed reps on a
+    bounded sample of the batch; None when the reference package is not shipped."""
+    import numpy as np
+
+    path = os.path.join(ROOT, "baseline", "_ref")
+    if not os.path.isdir(os.path.join(path, "fvbatch")):
+        return None
+    if path not in sys.path:
+        sys.path.append(path)
+    try:
+        import fvbatch.kernel as rk
+        import fvbatch.mesh as rm
+        import fvbatch.pde as rp
+        from fvbatch.kernel import vectorized
+    except Exception as exc:   # pragma: no cover
+        return {"unavailable": f"import failed: {exc}"}
+    # vectorized.py:254-255 names five undefined module attributes on every BATCHED
+    # variant (SURVEY.md Appendix B.1); binding them is the shim SURVEY §8d prescribes
+    for name in ("_pass_copy_args", "_pass_eig_args", "_pass_diss_args", "_pass_fluxfill_args",
+                 "_pass_fluxacc_args"):
+        if not hasattr(vectorized, name):
+            setattr(vectorized, name, None)
+    cores = cpu_cores()
+    m = min(qin.shape[0], 1024 if (dim == 3 and p >= 16) else (16384 if p >= 16 else 65536))
+    if os.environ.get("FVB_BENCH_CPU_SMALL"):
+        m = min(m, 8)
+    spec = rm.PatchSpec(dim, p, dim + 2)
+    b = rm.make_patch_batch(spec, m)
+    b.QIn[...] = qin[:m]
+    b.cell_size[...] = cs[:m]
+    b.dt[...] = dt[:m]
+    pd = rp.make_euler_pde(dim)
+    var = rk.variant_from_labels("batched", "aos", "par", worker_hint=cores)
+    rk.update_patch_batch(b, pd, var)
+    times = []
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        rk.update_patch_batch(b, pd, var)
+        times.append(time.perf_counter() - t0)
+    rm._offset_tensor.cache_clear() if hasattr(rm, "_offset_tensor") else None
+    med = statistics.median(times)
+    return {"value": m * p ** dim / med, "unit": "cell updates/s", "cores": cores, "kind": "reference",
+            "sample": f"fvbatch.kernel.update_patch_batch, batched/aos/par worker_hint={cores} (shimmed), "
+                      f"{m} patches, median of {reps} after 1 warm-up: {med:.2f} s"}
 
 
 def reference_arm(args):
-    """--impl reference: the reference algorithm on the host cores (oracle port), rank 0 only."""
+    """--impl reference: the reference algorithm on this box's host cores, rank 0 only.
+    Steps = the oracle port (the reference's update restated in C, OpenMP) over the
+    configuration's batch; the reference's own numpy engine is reported beside it."""
     if int(os.environ.get("RANK", "0")) != 0:
         return
-    dim, p, n_per_gpu, _ = CONFIGS[args.config]
-    per_step = []
-    value_total, cores, desc = None, None, None
-    budget = float(os.environ.get("FVB_BENCH_CPU_SECONDS", "20"))
-    for _ in range(args.warmup):
-        run_cpu_sample(dim, p, target_s=min(1.0, budget / 10))
-    for _ in range(args.steps):
-        v, cores, desc = run_cpu_sample(dim, p, target_s=max(budget / max(args.steps, 1), 0.05))
-        per_step.append(v)
-    value_total = statistics.median(per_step)
+    dim, p, n, cfg_idx = CONFIGS[args.config]
+    if os.environ.get("FVB_BENCH_CPU_SMALL"):   # CPU test suite: a tiny batch
+        n = min(n, 64)
+    qin, cs, dt = host_batch(dim, p, n)
+    budget = float(os.environ.get("FVB_BENCH_CPU_SECONDS", "60"))
+    rates, cores, m, ms = oracle_steps(qin, cs, dt, dim, p, args.steps, args.warmup, budget)
+    value = statistics.median(rates)
+    numpy_ref = None if os.environ.get("FVB_BENCH_NO_NUMPY") else numpy_engine_baseline(qin, cs, dt, dim, p)
+    sample = (f"oracle port (C restatement of vectorized.py, OpenMP, {cores} threads): {args.steps} steps of "
+              f"{m} patches each ({'the full batch' if m == n else 'rotating slices of the batch'})")
     line = {
-        "metric": METRIC, "impl": "reference", "value": value_total, "unit": "cell updates/s",
+        "metric": METRIC, "impl": "reference", "value": value, "unit": "cell updates/s",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": n_per_gpu * p ** dim / value_total * 1e3, "higher_is_better": True, "scaling": "weak",
+        "ms_per_step": statistics.median(ms), "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": f"{dim}D Euler p={p}, {n_per_gpu} patches ({_cfg_label(CONFIGS[args.config][3])})",
-                   "dim": dim, "p": p, "patches": n_per_gpu},
-        "cpu_baseline": {"value": value_total, "unit": "cell updates/s", "cores": cores, "kind": "port",
-                         "sample": desc},
-        "e2e": {"value": value_total, "unit": "cell updates/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "config": {"workload": f"{dim}D Euler p={p}, {n} patches ({_cfg_label(cfg_idx)})",
+                   "dim": dim, "p": p, "patches": n, "patches_per_step": m},
+        "cpu_baseline": {"value": value, "unit": "cell updates/s", "cores": cores, "kind": "port", "sample": sample},
+        "cpu_baseline_numpy": numpy_ref,
+        "e2e": {"value": value, "unit": "cell updates/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
 
@@ -232,11 +321,15 @@ def main():
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--config", default="c3", choices=sorted(CONFIGS))
+    ap.add_argument("--mode", default="fast", choices=["fast", "exact"])
     ap.add_argument("--layout", default="aos", choices=["aos", "soa"])
     ap.add_argument("--kernel", default="auto", choices=["auto", "fused", "generic"])
     ap.add_argument("--e2e-steps", type=int, default=8)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-exact-leg", action="store_true")
+    ap.add_argument("--no-graph", action="store_true")
     ap.add_argument("--scaling", default="weak", choices=["weak", "strong"])
+    ap.add_argument("--patches", type=int, default=None, help="override the patches per GPU (overhead studies)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
@@ -248,7 +341,6 @@ def main():
     import torch
     import torch.distributed as dist
 
-    import oracle  # cpu_baseline leg only
     from paper_2302_09005_b200 import device as fdev
     from paper_2302_09005_b200 import driver, mesh, pde
     from paper_2302_09005_b200.kernel import update_patch_batch, variant_from_labels
@@ -261,6 +353,8 @@ def main():
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 
     dim, p, n, cfg_idx = CONFIGS[args.config]
+    if args.patches:
+        n = args.patches
     n_total = n * world   # weak: every rank the configuration's count
     if args.scaling == "strong":   # the configuration's patches shared by the ranks
         lo, hi = driver.shard_bounds(n, rank, world)
@@ -288,62 +382,84 @@ def main():
         del qin_aos, qv
     db.cell_size.fill_(1.0)
     stream = torch.cuda.current_stream()
-    stepper = driver.CflStepper(db, cfl=0.4, dx=1.0 / p, kernel=args.kernel, stream=stream)
-    stepper.prepass()
-    torch.cuda.synchronize()
-    if db.nonphysical():
-        raise RuntimeError("synthetic input is not admissible")
-
-    for _ in range(args.warmup):
-        stepper.step()
     kernel_name = fdev.selected_kernel(dim, p, n, gamma, args.layout) if args.kernel == "auto" else args.kernel
 
-    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
-    t_start = torch.cuda.Event(enable_timing=True)
-    t_end = torch.cuda.Event(enable_timing=True)
-    if world > 1:
-        dist.barrier()
-    torch.cuda.synchronize()
-    with ClockSampler(local) as clocks:
-        t_start.record(stream)
-        for k in range(args.steps):
-            ev[k][0].record(stream)
-            db.update(kernel=args.kernel, stream=stream)
-            ev[k][1].record(stream)
-            stepper.reduce_dt()
-        t_end.record(stream)
+    def run_mode(mode, steps, warmup, clocks_ok):
+        """(total ms of `steps` graph-replayed steps, mean update-launch ms, redo count seen)."""
+        stepper = driver.CflStepper(db, cfl=0.4, dx=1.0 / p, kernel=args.kernel, stream=stream, mode=mode,
+                                    graph=not args.no_graph)
+        stepper.prepass()
         torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
-    total_ms = t_start.elapsed_time(t_end)
-    kern_ms = statistics.mean(a.elapsed_time(b) for a, b in ev)
-    if world > 1:
-        t = torch.tensor([total_ms, kern_ms], dtype=torch.float64, device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        total_ms, kern_ms = float(t[0]), float(t[1])
-    if db.nonphysical():
-        raise RuntimeError("non-physical state during the timed steps")
-    cells_per_gpu = n * p ** dim
-    total_cells = n_total * p ** dim
-    value = total_cells * args.steps / (total_ms * 1e-3)
-    ms_per_step = total_ms / args.steps
+        if db.nonphysical():
+            raise RuntimeError("synthetic input is not admissible")
+        for _ in range(warmup):
+            stepper.step()
+        t0 = torch.cuda.Event(enable_timing=True)
+        t1 = torch.cuda.Event(enable_timing=True)
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        t0.record(stream)
+        for _ in range(steps):
+            stepper.step()
+        t1.record(stream)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        total = t0.elapsed_time(t1)
+        # the update launch alone (fused kernel + its redo pass), event-bracketed on its stream
+        kn = min(steps, 50)
+        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(kn)]
+        for a, b in ev:
+            a.record(stream)
+            db.update(kernel=args.kernel, stream=stream, zero_status=False, mode=mode)
+            b.record(stream)
+        torch.cuda.synchronize()
+        kern = statistics.mean(a.elapsed_time(b) for a, b in ev)
+        if world > 1:
+            t = torch.tensor([total, kern], dtype=torch.float64, device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            total, kern = float(t[0]), float(t[1])
+        if db.nonphysical():
+            raise RuntimeError("non-physical state during the timed steps")
+        return total, kern
 
     peaks, peak_kind = measured_peaks()
     bytes_per_launch = n * algorithmic_bytes_per_patch(dim, p)
     flops_cell = algorithmic_flops_per_cell(dim, p)
-    achieved = bytes_per_launch / (kern_ms * 1e-3) / 1e9
+    cells_per_gpu = n * p ** dim
+    total_cells = n_total * p ** dim
+
+    def roofline(kern_ms):
+        achieved = bytes_per_launch / (kern_ms * 1e-3) / 1e9
+        return {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                "frac": achieved / peaks["hbm_gbs"], "kernel_ms": kern_ms,
+                "algorithmic_bytes_per_launch": bytes_per_launch,
+                "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_kind}, copy bandwidth)"}
+
+    with ClockSampler(torch, local) as clocks:
+        total_ms, kern_ms = run_mode(args.mode, args.steps, args.warmup, True)
+        exact = None
+        if args.mode == "fast" and not args.no_exact_leg:
+            ex_total, ex_kern = run_mode("exact", args.steps, args.warmup, True)
+            exact = {"value": total_cells * args.steps / (ex_total * 1e-3), "ms_per_step": ex_total / args.steps,
+                     "roofline": roofline(ex_kern), "mode": MODE_NOTE["exact"]}
+    value = total_cells * args.steps / (total_ms * 1e-3)
+    ms_per_step = total_ms / args.steps
+    roof = roofline(kern_ms)
     traffic = None
     prof = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(prof):
         try:
             with open(prof) as f:
-                traffic = json.load(f).get(f"{args.config}_{args.layout}", {}).get("dram_bytes_per_launch")
+                traffic = json.load(f).get(f"{args.config}_{args.layout}_{args.mode}", {}).get("dram_bytes_per_launch")
         except (OSError, ValueError):
             traffic = None
+    roof["traffic"] = traffic
 
     # ---- e2e: the drop-in public API on pinned host buffers ----
-    e2e = None
-    if args.e2e_steps > 0:
+    e2e, host = None, None
+    if args.e2e_steps > 0 or (rank == 0 and world == 1 and not args.no_cpu_baseline):
         host = mesh.make_patch_batch(spec, n, pinned=True)
         aos = db.QIn if args.layout == "aos" else None
         if aos is None:
@@ -354,10 +470,11 @@ def main():
                                               fdev._stream_handle(torch, stream)), "unpack")
         host.QIn.reshape(-1)[...] = aos.cpu().numpy()
         host.dt[...] = 0.4 * (1.0 / p) / 3.4
+    if args.e2e_steps > 0:
         euler = pde.make_euler_pde(dim)
         variant = variant_from_labels("batched", "aos", "par")
         for _ in range(2):   # warm-up (workspace allocation, first touch of the pinned pages)
-            update_patch_batch(host, euler, variant)
+            update_patch_batch(host, euler, variant, mode=args.mode)
         if world > 1:
             dist.barrier()
         torch.cuda.synchronize()
@@ -366,7 +483,7 @@ def main():
         e0.record(stream)
         t0 = time.perf_counter()
         for _ in range(args.e2e_steps):
-            update_patch_batch(host, euler, variant)
+            update_patch_batch(host, euler, variant, mode=args.mode)
         e1.record(stream)
         torch.cuda.synchronize()
         wall_ms = (time.perf_counter() - t0) * 1e3
@@ -388,14 +505,18 @@ def main():
         bound = total_cells / t_bound
         e2e["pcie_gbs"] = {k: round(v, 2) for k, v in bw.items()}
         e2e["roofline"] = {"bound": "pcie", "value": bound, "frac": e2e["value"] / bound}
-        del host
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        v, cores, desc = run_cpu_sample(dim, p)
-        cpu = {"value": v, "unit": "cell updates/s", "cores": cores, "kind": "port", "sample": desc}
+        budget = float(os.environ.get("FVB_BENCH_CPU_SECONDS", "10"))
+        rates, cores, m, _ = oracle_steps(host.QIn, host.cell_size, host.dt, dim, p, 3, 1, budget)
+        cpu = {"value": statistics.median(rates), "unit": "cell updates/s", "cores": cores, "kind": "port",
+               "sample": f"oracle port (C, OpenMP, {cores} threads) on this run's batch: 3 steps of {m} patches "
+                         f"({'the full batch' if m == n else 'rotating slices'}), median"}
+    del host
 
     if rank == 0:
+        launches_per_step = (2 if kernel_name == "fused" else 1) + (1 if (n <= 16384 and world == 1) else 2)
         line = {
             "metric": METRIC, "value": value, "unit": "cell updates/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": args.scaling,
@@ -405,24 +526,24 @@ def main():
                                     f"{dim}D Euler p={p}, {n_total} patches over {world} GPU(s) "
                                     f"({_cfg_label(cfg_idx)}, strong scaling)"),
                        "dim": dim, "p": p, "patches_per_gpu": n, "layout": args.layout, "kernel": kernel_name,
+                       "mode": MODE_NOTE[args.mode],
+                       "step": "CflStepper: update + redo + max-reduce/dt (+ NCCL MAX all-reduce)"
+                               + ("" if args.no_graph else ", CUDA-graph replay"),
                        "parallelism": f"patch shards x{world}, NCCL MAX all-reduce of the wave speed",
-                       "l2": f"inputs {n * spec.haloed_volumes * spec.unknowns * 8 / 1e6:.0f} MB > 126 MB L2; no flush"},
-            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
-                         "frac": achieved / peaks["hbm_gbs"], "traffic": traffic,
-                         "kernel_ms": kern_ms, "algorithmic_bytes_per_launch": bytes_per_launch,
-                         "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_kind})"},
-            # the min(HBM, FP64) roofline of the north star: the FP64 side at the algorithmic
-            # flop count (the exact recipe issues ~1.3x more FP64 instructions)
+                       "l2": f"inputs {n * spec.haloed_volumes * spec.unknowns * 8 / 1e6:.0f} MB vs 126 MB L2; "
+                             "no flush"},
+            "roofline": roof,
+            # the min(HBM, FP64) roofline of the north star: the FP64 side at the algorithmic flop count
             "roofline_fp64": {"achieved": flops_cell * cells_per_gpu / (kern_ms * 1e-3) / 1e12,
                               "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
                               "frac": flops_cell * cells_per_gpu / (kern_ms * 1e-3) / 1e12 / FP64_PEAK_TFLOPS,
-                              "flops_per_cell": flops_cell,
-                              "cells_per_s_at_peak": FP64_PEAK_TFLOPS * 1e12 / flops_cell},
+                              "flops_per_cell": flops_cell},
+            "exact": exact,
             "cpu_baseline": cpu,
             "e2e": e2e,
-            # per step: the update kernel (+ the fused path's redo pass) + the dt reduction
-            # (one kernel up to 16,384 patches, else reduce_max_grid + set_dt)
-            "gpu_launches": args.steps * ((2 if kernel_name == "fused" else 1) + (1 if n <= 16384 else 2)),
+            # per timed step: the update kernel (+ the fused path's redo pass) and the dt reduction
+            # (one kernel up to 16,384 patches on one GPU, else reduce + set_dt)
+            "gpu_launches": args.steps * launches_per_step,
             "clocks": clocks.summary(),
         }
         print(json.dumps(line), flush=True)

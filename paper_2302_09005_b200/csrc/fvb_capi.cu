@@ -115,7 +115,7 @@ int fvb_update(const fvb_spec* spec, const double* qin, double* qout, const doub
   return FVB_OK;
 }
 
-static size_t status_bytes(int64_t chunk) { return ((size_t)(2 * chunk + 2) * 4 + 255) / 256 * 256; }
+static size_t status_bytes(int64_t chunk) { return ((size_t)(2 * chunk + 3) * 4 + 255) / 256 * 256; }
 static size_t align256(size_t b) { return (b + 255) / 256 * 256; }
 // One buffer set of the host pipeline: qin, qout, cell_size, dt, max_eig, each
 // 256-byte aligned (the fused kernels move patches with TMA bulk copies, which
@@ -126,7 +126,7 @@ static size_t host_set_bytes(const fvb_spec* spec, int64_t chunk) {
          align256((size_t)chunk * spec->dim * 8) + 2 * align256((size_t)chunk * 8);
 }
 
-size_t fvb_status_words(int64_t n_patches) { return (size_t)(2 * n_patches + 2); }
+size_t fvb_status_words(int64_t n_patches) { return (size_t)(2 * n_patches + 3); }
 
 size_t fvb_update_host_workspace(const fvb_spec* spec, int64_t chunk) {
   if (check_spec(spec) || chunk < 1) return 0;
@@ -194,8 +194,9 @@ int fvb_update_host(const fvb_spec* spec, const double* qin_h, double* qout_h, c
   cudaEvent_t* ev_k = pp.ev_k;
   cudaEvent_t* ev_out = pp.ev_out;
   // flag words of both status buffers accumulate over the chunks; redo counts are reset per chunk
-  if (e == cudaSuccess) e = cudaMemsetAsync(status_b[0], 0, 8, comp);
-  if (e == cudaSuccess) e = cudaMemsetAsync(status_b[1], 0, 8, comp);
+  // both status buffers whole (flag, list, the redo kernel's CTA counter): the workspace
+  // is caller memory of unknown content
+  if (e == cudaSuccess) e = cudaMemsetAsync(status_b[0], 0, 2 * status_bytes(chunk), comp);
   // the copy streams must not run ahead of the status reset / earlier work on `comp`
   cudaEvent_t ev_start = pp.ev_start;
   if (e == cudaSuccess) e = cudaEventRecord(ev_start, comp);
@@ -217,8 +218,6 @@ int fvb_update_host(const fvb_spec* spec, const double* qin_h, double* qout_h, c
     if (e != cudaSuccess) break;
     fvb_spec sub = *spec;
     sub.n_patches = np;
-    e = cudaMemsetAsync(status_b[b] + 1, 0, 4, comp);   // redo count of this chunk
-    if (e != cudaSuccess) break;
     krc = fvb_update(&sub, qin_d[b], qout_d[b], cs_d[b], dt_d[b], me_d[b], status_b[b], kernel, 0, stream);
     if (krc != FVB_OK) break;
     e = cudaEventRecord(ev_k[b], comp);

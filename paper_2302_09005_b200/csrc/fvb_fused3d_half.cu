@@ -20,10 +20,10 @@
 // haloed row y0 + r; interior local row ly (0..7) is stage row ly + 1.
 //
 // Per-patch outputs: each half writes its 8 x 16 cells of every interior plane
-// with a TMA bulk store; the patch's max_eigenvalue is the atomicMax of the two
-// halves' maxima on the bit patterns (max_eig is zeroed by the launcher).  A
-// half whose volumes leave the range gate queues its patch for the exact redo
-// pass (a patch can be queued twice, see fvb_status_words).
+// with a TMA bulk store.  A CTA processes both halves of its patches back to
+// back, so it writes the patch's max_eigenvalue (the max of the two halves'
+// maxima on the bit patterns) and, when a volume of either half left the range
+// gate, queues the patch once for the exact redo pass.
 #include <cuda_runtime.h>
 
 #include <type_traits>
@@ -141,14 +141,17 @@ fused3d_half_kernel(const double* __restrict__ qin, double* __restrict__ qout, c
   const int ly = (warp << 1) | (lane >> 4);   // local interior row 0..R-1 (interior warps)
   const bool producer = tid == 32 * NIW;
 
-  const int64_t items = IPP * n;   // (patch, row block) work items
-  const int my_items = (items > (int64_t)blockIdx.x) ? (int)((items - 1 - (int64_t)blockIdx.x) / gridDim.x + 1) : 0;
-  auto item_index = [&](int j) -> int64_t { return (int64_t)blockIdx.x + (int64_t)j * gridDim.x; };
+  // Work items: the CTA's patches blockIdx.x + i * gridDim.x, each as its IPP row blocks
+  // back to back (item j = patch j / IPP, rows (j % IPP) * R ..), so one CTA sees every
+  // row block of its patches and writes max_eigenvalue / the redo entry itself -- no
+  // zero-initialised max_eig (atomicMax) and no duplicate redo entries.
+  const int my_patches = (n > (int64_t)blockIdx.x) ? (int)((n - 1 - (int64_t)blockIdx.x) / gridDim.x + 1) : 0;
+  const int my_items = IPP * my_patches;
+  auto item_patch = [&](int j) -> int64_t { return (int64_t)blockIdx.x + (int64_t)(j / IPP) * gridDim.x; };
 
   auto issue = [&](int j, int zh, unsigned s) {
-    const int64_t it = item_index(j);
-    const int64_t pidx = it / IPP;
-    const int y0 = (int)(it % IPP) * R;
+    const int64_t pidx = item_patch(j);
+    const int y0 = (j % IPP) * R;
     double* st = ring + s * STAGE;
     uint64_t* bar = bars + s;
     fence_proxy_async();
@@ -174,18 +177,25 @@ fused3d_half_kernel(const double* __restrict__ qin, double* __restrict__ qout, c
     }
     bulk_commit();
   };
-  auto finish_item = [&](int j, int64_t pidx) {
-    unsigned long long m = wmax[(j & 1) * NIW];
+  auto finish_patch = [&](int j, int64_t pidx) {   // after the patch's last row block, item j
+    static_assert(IPP <= 2, "wmax / slowflag hold two items");
+    unsigned long long m = 0;
+    unsigned slow_any = 0;
 #pragma unroll
-    for (int w = 1; w < NIW; ++w) {
-      const unsigned long long v = wmax[(j & 1) * NIW + w];
-      m = v > m ? v : m;
+    for (int i = 0; i < IPP; ++i) {
+      const int par = (j - i) & 1;
+#pragma unroll
+      for (int w = 0; w < NIW; ++w) {
+        const unsigned long long v = wmax[par * NIW + w];
+        m = v > m ? v : m;
+      }
+      slow_any |= slowflag[par];
+      slowflag[par] = 0;
     }
-    atomicMax(reinterpret_cast<unsigned long long*>(max_eig) + pidx, m);
-    if (slowflag[j & 1]) {   // queue the patch for the exact re-evaluation (fvb_redo_kernel)
+    reinterpret_cast<unsigned long long*>(max_eig)[pidx] = m;
+    if (slow_any) {   // queue the patch for the exact re-evaluation (fvb_redo_kernel)
       const unsigned k = atomicAdd(&status[1], 1u);
       status[2 + k] = (unsigned)pidx;
-      slowflag[j & 1] = 0;
     }
   };
 
@@ -217,9 +227,8 @@ fused3d_half_kernel(const double* __restrict__ qin, double* __restrict__ qout, c
   static_assert(NPL % (2 * NST) == 0, "stage / parity must be item-periodic");
 
   for (int jp = 0; jp < my_items; ++jp) {
-    const int64_t it = item_index(jp);
-    const int64_t pidx = it / IPP;
-    const int y0 = (int)(it % IPP) * R;
+    const int64_t pidx = item_patch(jp);
+    const int y0 = (jp % IPP) * R;
     const double dx = __ddiv_rn(cell_size[pidx * 3], (double)P);   // vectorized.py:169
     const double inv = __ddiv_rn(dtv[pidx], dx);                    // vectorized.py:170
     const double half_inv = dmul(0.5, inv);
@@ -373,7 +382,7 @@ fused3d_half_kernel(const double* __restrict__ qin, double* __restrict__ qout, c
         const int jn = zh + 2 < NPL ? jp : jp + 1;
         if (jn < my_items) issue(jn, zn, stp);
         if (K == kSteady || K == kZHi) store_out(pidx, y0, zh - 2);
-        if (K == kZHi) finish_item(jp, pidx);
+        if (K == kZHi && jp % IPP == IPP - 1) finish_patch(jp, pidx);
       }
     };
 
@@ -392,8 +401,6 @@ cudaError_t launch_impl(const FvbArgs& a, cudaStream_t st) {
   auto kfn = fused3d_half_kernel<L>;
   cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)BYTES);
   if (e != cudaSuccess) return e;
-  e = cudaMemsetAsync(a.max_eig, 0, sizeof(double) * (size_t)a.n, st);   // atomicMax of the two halves
-  if (e != cudaSuccess) return e;
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -401,7 +408,7 @@ cudaError_t launch_impl(const FvbArgs& a, cudaStream_t st) {
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kfn, NTHREADS, BYTES);
   if (per_sm < 1) per_sm = 1;
   int64_t grid = (int64_t)sms * per_sm;
-  if (grid > IPP * a.n) grid = IPP * a.n;
+  if (grid > a.n) grid = a.n;
   const Closure cl{a.gamma, a.gamma - 1.0};
   kfn<<<(unsigned)grid, NTHREADS, BYTES, st>>>(a.qin, a.qout, a.cell_size, a.dt, a.max_eig, a.status, a.n, cl);
   return cudaGetLastError();

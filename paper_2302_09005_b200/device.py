@@ -143,7 +143,7 @@ class DeviceBatch:
 
     def update_range(self, p0: int, p1: int, kernel="auto", stream=None, mode: str = "exact") -> None:
         """The update of patches [p0, p1) only (a contiguous sub-batch: same buffers, offset
-        pointers; the status flag accumulates, the redo count is reset for this launch).
+        pointers; the status flag accumulates, the redo list empties itself).
         run_simulation_sharded updates its boundary layers first with it, so their exchange
         overlaps the update of the interior layers."""
         torch = _torch()
@@ -154,7 +154,6 @@ class DeviceBatch:
         sub = _lib.spec(d, self.spec.volumes_per_axis, p1 - p0, self.gamma, LAYOUTS[self.layout])
         if self.layout != "aos":
             raise ContractViolationError("update_range: AoS batches only")
-        self.status[1:2].zero_()
         _lib.check(_lib.load().fvb_update(
             ctypes.byref(sub), _vp(self.QIn[p0 * V * s:]), _vp(self.QOut[p0 * I * s:]),
             _vp(self.cell_size[p0 * d:]), _vp(self.dt[p0:]), _vp(self.max_eigenvalue[p0:]), _vp(self.status),

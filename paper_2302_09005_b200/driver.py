@@ -50,28 +50,41 @@ def shard_bounds(n: int, rank: int, world: int) -> tuple[int, int]:
 
 
 class CflStepper:
-    """Device-resident step loop for one shard."""
+    """Device-resident step loop for one shard: update -> local max wave speed ->
+    (NCCL MAX all-reduce) -> dt, every step enqueued without a host synchronisation.
+
+    The redo list of the fused kernels empties itself (fvb_status_words), so a step
+    issues no memset: 2 kernels on one GPU for up to 16,384 patches (the fused update
+    with its redo pass, and one reduce+dt kernel), plus the all-reduce on N GPUs.
+    graph=True captures that step once in a CUDA graph and replays it, which removes the
+    per-launch host cost (ctypes + driver) from small-shard strong scaling."""
 
     def __init__(self, db: DeviceBatch, cfl: float = 0.4, dx: float | None = None, group=None,
-                 kernel="auto", stream=None):
+                 kernel="auto", stream=None, mode: str = "exact", graph: bool = False):
         torch = _torch()
         self.db = db
         self.cfl = float(cfl)
         self.dx = float(dx) if dx is not None else float(db.cell_size[0].item()) / db.spec.volumes_per_axis
         self.group = group
         self.kernel = kernel
+        self.mode = mode
         self.stream = stream
+        self.use_graph = bool(graph)
+        self._graph = None
         self.gmax = torch.zeros(1, dtype=torch.float64, device=db.device)
         self.dt_scalar = torch.zeros(1, dtype=torch.float64, device=db.device)
         import torch.distributed as dist
 
         self._dist = dist if (dist.is_available() and dist.is_initialized()) else None
 
-    def reduce_dt(self) -> None:
+    def _multi(self) -> bool:
+        return self._dist is not None and self._dist.get_world_size(self.group) > 1
+
+    def reduce_dt(self, stream=None) -> None:
         torch = _torch()
         L = _lib.load()
-        st = _stream_handle(torch, self.stream)
-        if self._dist is None or self._dist.get_world_size(self.group) == 1:
+        st = _stream_handle(torch, stream if stream is not None else self.stream)
+        if not self._multi():
             _lib.check(L.fvb_reduce_dt(_vp(self.db.max_eigenvalue), self.db.n_patches, self.cfl, self.dx,
                                        _vp(self.gmax), _vp(self.dt_scalar), _vp(self.db.dt), 1, st), "fvb_reduce_dt")
             return
@@ -82,14 +95,31 @@ class CflStepper:
                                 self.db.n_patches, st), "fvb_set_dt")
 
     def prepass(self) -> None:
-        """First-step dt from the initial wave speeds."""
+        """First-step dt from the initial wave speeds; clears the status words."""
+        self.db.status.zero_()
         self.db.max_eig_prepass(stream=self.stream)
         self.reduce_dt()
 
+    def _enqueue(self, stream) -> None:
+        self.db.update(kernel=self.kernel, stream=stream, zero_status=False, mode=self.mode)
+        self.reduce_dt(stream)
+
     def step(self) -> None:
-        """update -> local max -> (all-reduce) -> dt, all enqueued on the stream."""
-        self.db.update(kernel=self.kernel, stream=self.stream)
-        self.reduce_dt()
+        """update -> local max -> (all-reduce) -> dt, enqueued on the stream (or replayed)."""
+        if not self.use_graph:
+            self._enqueue(self.stream)
+            return
+        torch = _torch()
+        if self._graph is None:
+            self._enqueue(self.stream)   # one eager step: lazy library / NCCL setup before capture
+            side = torch.cuda.Stream(device=self.db.device)
+            side.wait_stream(self.stream if self.stream is not None else torch.cuda.current_stream())
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, stream=side):
+                self._enqueue(None)      # the capture stream is current inside the context
+            self._graph = g
+            return
+        self._graph.replay()
 
 
 def cfl_dt(db: DeviceBatch, cfl: float = 0.4, dx: float | None = None, group=None):
@@ -188,7 +218,6 @@ def run_simulation(db: DeviceBatch, grid_shape, steps: int, cfl: float = 0.4, pe
         st = _sh(torch, None)
         src, dst = bufs[k % 2], bufs[(k + 1) % 2]
         dt_h.index_copy_(0, k_t, stepper.dt_scalar)
-        db.status[1:2].zero_()
         _lib.check(L.fvb_update_to_haloed(fs, _vp(src), _vp(dst), _vp(db.cell_size), _vp(db.dt),
                                           _vp(db.max_eigenvalue), _vp(db.status), 0, st), "fvb_update_to_haloed")
         flag_h.index_copy_(0, k_t, db.status[0:1])
@@ -201,8 +230,7 @@ def run_simulation(db: DeviceBatch, grid_shape, steps: int, cfl: float = 0.4, pe
 
     def step_body():
         dt_h.index_copy_(0, k_t, stepper.dt_scalar)       # the dt this step advances by
-        db.status[1:2].zero_()                            # redo count of this launch; status[0] accumulates
-        db.update(kernel=kernel, zero_status=False)
+        db.update(kernel=kernel, zero_status=False)       # status[0] accumulates; the redo list self-empties
         flag_h.index_copy_(0, k_t, db.status[0:1])
         stepper.reduce_dt()                               # next step's dt from this step's wave speeds
         db.halo_project_totals(grid_shape, periodic, tot_cur, scratch)   # one pass over QOut
@@ -436,7 +464,6 @@ def run_simulation_sharded(sg: ShardedGrid, steps: int, cfl: float = 0.4, kernel
     gmax_h[0].copy_(stepper.gmax[0])
     for k in range(steps):
         dt_h[k].copy_(stepper.dt_scalar[0])
-        db.status[1:2].zero_()
         sg.update_and_exchange(kernel)        # boundary layers first, their exchange overlaps the rest
         flag_h[k].copy_(db.status[0])
         stepper.reduce_dt()
