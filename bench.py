@@ -17,8 +17,9 @@ Rank 0 prints one JSON line (the driver contract):
   e2e          the drop-in public API (kernel.update_patch_batch) on pinned host
                arrays, H2D + D2H inside the timed region
   roofline     the update kernel's algorithmic HBM bytes per launch over its
-               event-timed duration (an eager pass of the same launches right after
-               the timed region) against MEASURED_PEAKS.json
+               duration, timed by CUDA events around every update inside the
+               replayed graph (the last graph of the timed region), against
+               MEASURED_PEAKS.json
   cpu_baseline the CPU oracle (a C restatement of the reference algorithm, oracle/)
                over the full configuration batch, on this box's host cores
 """
@@ -392,6 +393,14 @@ def main():
         torch.cuda.synchronize()
         if db.nonphysical():
             raise RuntimeError("synthetic input is not admissible")
+        # the timed steps: m-step CUDA graphs (m divides K), each step's update launch
+        # (fused kernel + its redo pass) bracketed by timing events inside the graph
+        m = max(d for d in range(1, min(steps, 32) + 1) if steps % d == 0)
+        graph = None
+        if args.no_graph:
+            ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(m)]
+        else:
+            graph, ev = stepper.make_graph(m, timing=True)
         for _ in range(warmup):
             stepper.step()
         t0 = torch.cuda.Event(enable_timing=True)
@@ -400,22 +409,21 @@ def main():
             dist.barrier()
         torch.cuda.synchronize()
         t0.record(stream)
-        for _ in range(steps):
-            stepper.step()
+        for _ in range(steps // m):
+            if graph is not None:
+                graph.replay()
+                continue
+            for a, b in ev:
+                a.record(stream)
+                db.update(kernel=args.kernel, stream=stream, zero_status=False, mode=mode)
+                b.record(stream)
+                stepper.reduce_dt()
         t1.record(stream)
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
         total = t0.elapsed_time(t1)
-        # the update launch alone (fused kernel + its redo pass), event-bracketed on its stream
-        kn = min(steps, 50)
-        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(kn)]
-        for a, b in ev:
-            a.record(stream)
-            db.update(kernel=args.kernel, stream=stream, zero_status=False, mode=mode)
-            b.record(stream)
-        torch.cuda.synchronize()
-        kern = statistics.mean(a.elapsed_time(b) for a, b in ev)
+        kern = statistics.mean(a.elapsed_time(b) for a, b in ev)   # the last m steps of the timed region
         if world > 1:
             t = torch.tensor([total, kern], dtype=torch.float64, device="cuda")
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -516,7 +524,12 @@ def main():
     del host
 
     if rank == 0:
-        launches_per_step = (2 if kernel_name == "fused" else 1) + (1 if (n <= 16384 and world == 1) else 2)
+        # fvb_update_cfl: the update kernel, its redo pass carrying the max reduction (and on
+        # one GPU the dt) for <= 16,384 patches; else a grid reduce (+ set_dt); N GPUs: set_dt
+        if kernel_name == "fused" and n <= 16384:
+            launches_per_step = 2 + (1 if world > 1 else 0)
+        else:
+            launches_per_step = (2 if kernel_name == "fused" else 1) + 2
         line = {
             "metric": METRIC, "value": value, "unit": "cell updates/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": args.scaling,
@@ -527,7 +540,8 @@ def main():
                                     f"({_cfg_label(cfg_idx)}, strong scaling)"),
                        "dim": dim, "p": p, "patches_per_gpu": n, "layout": args.layout, "kernel": kernel_name,
                        "mode": MODE_NOTE[args.mode],
-                       "step": "CflStepper: update + redo + max-reduce/dt (+ NCCL MAX all-reduce)"
+                       "step": "CflStepper: fvb_update_cfl (update, redo pass with the max-reduce/dt) "
+                               "(+ NCCL MAX all-reduce + set_dt)"
                                + ("" if args.no_graph else ", CUDA-graph replay"),
                        "parallelism": f"patch shards x{world}, NCCL MAX all-reduce of the wave speed",
                        "l2": f"inputs {n * spec.haloed_volumes * spec.unknowns * 8 / 1e6:.0f} MB vs 126 MB L2; "

@@ -90,6 +90,16 @@ int fvb_update(const fvb_spec* spec, const double* qin, double* qout, const doub
                const double* dt, double* max_eig, uint32_t* status, int kernel, int zero_status,
                void* stream);
 
+/* fvb_update (zero_status = 0) followed by the CFL step control of the multi-step
+ * driver (no reference code): *gmax = max over the batch's max_eig
+ * (NaN wins, as numpy's max), and with set_dt, dt = (cfl*dx)/gmax into *dt_scalar and
+ * every dt[patch].  On the fused paths, for up to 16,384 patches, the reduction runs
+ * inside the update's redo pass (one CTA), so a step is two launches and no memset;
+ * otherwise the reduce kernels follow.  Asynchronous on `stream`. */
+int fvb_update_cfl(const fvb_spec* spec, const double* qin, double* qout, const double* cell_size,
+                   double* dt, double* max_eig, uint32_t* status, int kernel, double cfl, double dx,
+                   double* gmax, double* dt_scalar, int set_dt, void* stream);
+
 /* Number of uint32 status words fvb_update needs for n patches (2n + 3: flag,
  * redo count, redo list -- sized 2n for kernels that may queue a patch twice --
  * and the redo pass's CTA counter). */

@@ -28,7 +28,7 @@ KERNEL_FUSED = 2
 
 # Every symbol include/fvb200.h declares (checked by the CPU test suite).
 EXPORTED = (
-    "fvb_version", "fvb_strerror", "fvb_select_kernel", "fvb_update", "fvb_status_words",
+    "fvb_version", "fvb_strerror", "fvb_select_kernel", "fvb_update", "fvb_update_cfl", "fvb_status_words",
     "fvb_update_host_workspace", "fvb_update_host", "fvb_locate", "fvb_pack", "fvb_unpack",
     "fvb_reduce_dt", "fvb_set_dt", "fvb_patch_max_eig", "fvb_probe", "fvb_selftest_div",
     "fvb_halo_project", "fvb_halo_project_totals", "fvb_halo_project_window",
@@ -70,6 +70,8 @@ def load():
     L.fvb_select_kernel.argtypes = [sp]
     L.fvb_update.restype = i32
     L.fvb_update.argtypes = [sp, vp, vp, vp, vp, vp, vp, i32, i32, vp]
+    L.fvb_update_cfl.restype = i32
+    L.fvb_update_cfl.argtypes = [sp, vp, vp, vp, vp, vp, vp, i32, ctypes.c_double, ctypes.c_double, vp, vp, i32, vp]
     L.fvb_status_words.restype = ctypes.c_size_t
     L.fvb_status_words.argtypes = [i64]
     L.fvb_update_host_workspace.restype = ctypes.c_size_t

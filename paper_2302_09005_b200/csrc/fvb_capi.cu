@@ -70,8 +70,14 @@ int fvb_select_kernel(const fvb_spec* spec) {
   return resolve_kernel(spec, FVB_KERNEL_AUTO);
 }
 
-int fvb_update(const fvb_spec* spec, const double* qin, double* qout, const double* cell_size, const double* dt,
-               double* max_eig, uint32_t* status, int kernel, int zero_status, void* stream) {
+}  // extern "C"
+
+namespace {
+// fvb_update / fvb_update_cfl.  With tail != nullptr (fvb_update_cfl) the step also reduces
+// max_eig to *tail->gmax and optionally sets dt: inside the redo pass when the fused path
+// runs one and the batch is small enough for one CTA, else with the reduce kernels.
+int update_impl(const fvb_spec* spec, const double* qin, double* qout, const double* cell_size, double* dt,
+                double* max_eig, uint32_t* status, int kernel, int zero_status, const FvbArgs* tail, void* stream) {
   int rc = check_spec(spec);
   if (rc) return rc;
   if (spec->n_patches == 0) return FVB_OK;   // kernel/__init__.py:123-124
@@ -100,6 +106,15 @@ int fvb_update(const fvb_spec* spec, const double* qin, double* qout, const doub
   a.dt = dt;
   a.max_eig = max_eig;
   a.status = status;
+  const bool tail_in_redo = tail && k == FVB_KERNEL_FUSED && spec->n_patches <= kTailMaxPatches;
+  if (tail_in_redo) {
+    a.gmax = tail->gmax;
+    a.cfl = tail->cfl;
+    a.dx = tail->dx;
+    a.dt_scalar = tail->dt_scalar;
+    a.dt_patches = tail->tail_dt ? dt : nullptr;
+    a.tail_dt = tail->tail_dt;
+  }
   if (k == FVB_KERNEL_GENERIC) {
     // per-patch maxima are combined with atomicMax on the bit patterns
     e = cudaMemsetAsync(max_eig, 0, sizeof(double) * (size_t)spec->n_patches, st);
@@ -111,8 +126,33 @@ int fvb_update(const fvb_spec* spec, const double* qin, double* qout, const doub
   } else {
     e = fvb_launch_fused16(a, st);
   }
+  if (e == cudaSuccess && tail && !tail_in_redo)
+    e = fvb_launch_reduce_dt(max_eig, spec->n_patches, tail->cfl, tail->dx, tail->gmax, tail->dt_scalar,
+                             tail->tail_dt ? dt : nullptr, tail->tail_dt, st);
   if (e != cudaSuccess) return set_cuda_error(e, "fvb_update launch");
   return FVB_OK;
+}
+}  // namespace
+
+extern "C" {
+
+int fvb_update(const fvb_spec* spec, const double* qin, double* qout, const double* cell_size, const double* dt,
+               double* max_eig, uint32_t* status, int kernel, int zero_status, void* stream) {
+  return update_impl(spec, qin, qout, cell_size, const_cast<double*>(dt), max_eig, status, kernel, zero_status,
+                     nullptr, stream);
+}
+
+int fvb_update_cfl(const fvb_spec* spec, const double* qin, double* qout, const double* cell_size, double* dt,
+                   double* max_eig, uint32_t* status, int kernel, double cfl, double dx, double* gmax,
+                   double* dt_scalar, int set_dt, void* stream) {
+  if (!gmax) return set_contract("null gmax");
+  FvbArgs tail;
+  tail.gmax = gmax;
+  tail.cfl = cfl;
+  tail.dx = dx;
+  tail.dt_scalar = set_dt ? dt_scalar : nullptr;
+  tail.tail_dt = set_dt ? 1 : 0;
+  return update_impl(spec, qin, qout, cell_size, dt, max_eig, status, kernel, 0, &tail, stream);
 }
 
 static size_t status_bytes(int64_t chunk) { return ((size_t)(2 * chunk + 3) * 4 + 255) / 256 * 256; }

@@ -22,7 +22,16 @@ struct FvbArgs {
   double* max_eig;
   unsigned* status;
   int out_haloed = 0;   // 1: qout is a haloed AoS batch (N*V*S); the update fills its interior
+  // CFL tail (fvb_update_cfl): the redo pass's last CTA (or CTA 0 when the list is
+  // empty) reduces max_eig to *gmax and, with tail_dt, writes dt = (cfl*dx)/gmax
+  double* gmax = nullptr;
+  double cfl = 0.0, dx = 0.0;
+  double* dt_scalar = nullptr;
+  double* dt_patches = nullptr;
+  int tail_dt = 0;
 };
+
+constexpr int64_t kTailMaxPatches = 16384;   // one CTA reduces max_eig within the redo pass
 
 cudaError_t fvb_launch_generic(const FvbArgs& a, cudaStream_t st);
 cudaError_t fvb_launch_fused16(const FvbArgs& a, cudaStream_t st);

@@ -141,6 +141,17 @@ class DeviceBatch:
             _vp(self.max_eigenvalue), _vp(self.status), kernel_id(kernel, mode), int(zero_status),
             _stream_handle(torch, stream)), "fvb_update")
 
+    def update_cfl(self, cfl: float, dx: float, gmax, dt_scalar=None, kernel="auto", stream=None,
+                   mode: str = "exact") -> None:
+        """update() plus the CFL step control in the same launches (fvb_update_cfl): gmax <- max
+        wave speed of the batch; with dt_scalar, dt = (cfl*dx)/gmax into dt_scalar and self.dt."""
+        torch = _torch()
+        _lib.check(_lib.load().fvb_update_cfl(
+            ctypes.byref(self.fvb_spec()), _vp(self.QIn), _vp(self.QOut), _vp(self.cell_size), _vp(self.dt),
+            _vp(self.max_eigenvalue), _vp(self.status), kernel_id(kernel, mode), float(cfl), float(dx), _vp(gmax),
+            _vp(dt_scalar) if dt_scalar is not None else None, int(dt_scalar is not None),
+            _stream_handle(torch, stream)), "fvb_update_cfl")
+
     def update_range(self, p0: int, p1: int, kernel="auto", stream=None, mode: str = "exact") -> None:
         """The update of patches [p0, p1) only (a contiguous sub-batch: same buffers, offset
         pointers; the status flag accumulates, the redo list empties itself).

@@ -53,9 +53,10 @@ class CflStepper:
     """Device-resident step loop for one shard: update -> local max wave speed ->
     (NCCL MAX all-reduce) -> dt, every step enqueued without a host synchronisation.
 
-    The redo list of the fused kernels empties itself (fvb_status_words), so a step
-    issues no memset: 2 kernels on one GPU for up to 16,384 patches (the fused update
-    with its redo pass, and one reduce+dt kernel), plus the all-reduce on N GPUs.
+    The redo list of the fused kernels empties itself (fvb_status_words) and the max
+    reduction + dt run inside the update's redo pass (fvb_update_cfl), so a step is two
+    kernels and no memset on one GPU for up to 16,384 patches; on N GPUs the local max,
+    the all-reduce and fvb_set_dt.
     graph=True captures that step once in a CUDA graph and replays it, which removes the
     per-launch host cost (ctypes + driver) from small-shard strong scaling."""
 
@@ -101,8 +102,39 @@ class CflStepper:
         self.reduce_dt()
 
     def _enqueue(self, stream) -> None:
-        self.db.update(kernel=self.kernel, stream=stream, zero_status=False, mode=self.mode)
-        self.reduce_dt(stream)
+        """One step: fvb_update_cfl (update + redo pass + local max, and on one GPU the dt in
+        the same launches), then on N GPUs the all-reduce and fvb_set_dt."""
+        torch = _torch()
+        if not self._multi():
+            self.db.update_cfl(self.cfl, self.dx, self.gmax, self.dt_scalar, kernel=self.kernel,
+                               stream=stream if stream is not None else self.stream, mode=self.mode)
+            return
+        st = stream if stream is not None else self.stream
+        self.db.update_cfl(self.cfl, self.dx, self.gmax, None, kernel=self.kernel, stream=st, mode=self.mode)
+        allreduce_max_(self.gmax, self.group)
+        _lib.check(_lib.load().fvb_set_dt(_vp(self.gmax), self.cfl, self.dx, _vp(self.dt_scalar), _vp(self.db.dt),
+                                          self.db.n_patches, _stream_handle(torch, st)), "fvb_set_dt")
+
+    def make_graph(self, steps: int, timing: bool = False):
+        """Capture `steps` consecutive steps in one CUDA graph (replay with graph.replay()).
+        With timing=True every step's update is bracketed by its own pair of (external)
+        timing events, so the update kernels' durations can be read back after a replay:
+        returns (graph, [(start, end), ...])."""
+        torch = _torch()
+        self._enqueue(self.stream)   # lazy library / NCCL setup outside the capture
+        side = torch.cuda.Stream(device=self.db.device)
+        side.wait_stream(self.stream if self.stream is not None else torch.cuda.current_stream())
+        events = [(torch.cuda.Event(enable_timing=True, external=True),
+                   torch.cuda.Event(enable_timing=True, external=True)) for _ in range(steps if timing else 0)]
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=side):
+            for k in range(steps):
+                if timing:
+                    events[k][0].record()
+                self._enqueue(None)
+                if timing:
+                    events[k][1].record()
+        return g, events
 
     def step(self) -> None:
         """update -> local max -> (all-reduce) -> dt, enqueued on the stream (or replayed)."""

@@ -293,3 +293,59 @@ def test_update_range_split_matches_whole(dim, p, grid, monkeypatch):
     lo, hi = lay["patch_lo"], lay["patch_hi"]
     assert_bits_equal(sg.db.QOut.cpu().numpy(), whole.QOut.view(n, -1)[lo:hi].reshape(-1).cpu().numpy(), "QOut")
     assert_bits_equal(sg.db.max_eigenvalue.cpu().numpy(), whole.max_eigenvalue[lo:hi].cpu().numpy(), "max_eig")
+
+
+@pytest.mark.parametrize("dim,p,n,kernel,negzero", [(3, 16, 300, "auto", False), (3, 16, 40, "auto", True),
+                                                    (2, 16, 2000, "auto", False), (3, 4, 20000, "auto", False),
+                                                    (3, 7, 30, "generic", False), (2, 5, 64, "auto", True)])
+@pytest.mark.parametrize("mode", ["exact", "fast"])
+def test_update_cfl_tail_matches_host(dim, p, n, kernel, negzero, mode):
+    """fvb_update_cfl: QOut / max_eig as fvb_update, gmax = max(max_eig) and dt = (cfl*dx)/gmax
+    (fvb_set_dt's rounding) in every dt slot -- via the redo pass's tail (empty list: CTA 0;
+    queued patches: the last CTA), or the reduce kernels (generic kernel, > 16,384 patches)."""
+    b = mesh.make_patch_batch(mesh.PatchSpec(dim, p, dim + 2), n)
+    q = oracle.synthetic_qin(dim, p, n, seed=n + p).reshape(n, -1, dim + 2)
+    if negzero:
+        q[::3, ::7, 1] = -0.0      # leaves the range gate: those patches go through the redo list
+    b.QIn[...] = q.reshape(n, -1)
+    b.dt[...] = 0.4 * (1.0 / p) / 3.4
+    ref_q, ref_l, st = oracle.update(dim, p, 1.4, b.QIn, b.cell_size, b.dt)
+    assert st == 0
+    db = device.DeviceBatch.from_host(b, 1.4)
+    gmax = torch.zeros(1, dtype=torch.float64, device="cuda")
+    dts = torch.zeros(1, dtype=torch.float64, device="cuda")
+    for _ in range(2):   # twice: the redo list and its CTA counter must have reset themselves
+        db.dt.fill_(b.dt[0])
+        db.update_cfl(0.4, 1.0 / p, gmax, dts, kernel=kernel, mode=mode)
+        torch.cuda.synchronize()
+        assert int(db.status[1].item()) == 0 and int(db.status[-1].item()) == 0
+        out = mesh.make_patch_batch(b.spec, n)
+        db.to_host(out)
+        if mode == "exact" or not (dim == 3 and p == 16):
+            assert_bits_equal(out.QOut, ref_q, "QOut")
+        assert_bits_equal(out.max_eigenvalue, ref_l, "max_eig")
+        g = float(np.max(ref_l))
+        assert gmax.item() == g
+        dt = (0.4 * (1.0 / p)) / g
+        assert dts.item() == dt
+        assert np.all(db.dt.cpu().numpy() == dt)
+
+
+@pytest.mark.parametrize("mode", ["exact", "fast"])
+def test_cfl_stepper_graph_equals_eager(mode):
+    dim, p, n = 3, 16, 24
+    b = mesh.make_patch_batch(mesh.PatchSpec(dim, p, dim + 2), n)
+    b.QIn[...] = oracle.synthetic_qin(dim, p, n, seed=5)
+    res = []
+    for graph in (False, True):
+        db = device.DeviceBatch.from_host(b, 1.4)
+        st = driver.CflStepper(db, cfl=0.4, mode=mode, graph=graph)
+        st.prepass()
+        dts = []
+        for _ in range(4):   # the stepper re-reads the same QIn: every step is the same update
+            st.step()
+            dts.append(st.dt_scalar.item())
+        res.append((db.QOut.cpu().numpy(), db.max_eigenvalue.cpu().numpy(), dts))
+    assert_bits_equal(res[0][0], res[1][0], "QOut")
+    assert_bits_equal(res[0][1], res[1][1], "max_eig")
+    assert res[0][2] == res[1][2]
