@@ -77,14 +77,15 @@ int fvb_select_kernel(const fvb_spec* spec);
  *   cell_size  [N*dim]  only cell_size[patch*dim + 0] is read (vectorized.py:169)
  *   dt         [N]      per-patch time step, must be >= 0 (checked by the host)
  *   max_eig    [N]      per-patch max directional wave speed (written, vectorized.py:226-231)
- *   status     [2N+3]   device words (fvb_status_words), zero-initialised once by the caller:
+ *   status     [2N+5]   device words (fvb_status_words), zero-initialised once by the caller:
  *                       status[0] is ORed with 1 when a face-box volume has rho <= 0 or
  *                       p < 0 (sticky: clear it with zero_status = 1 or a memset);
  *                       status[1] / status[2..2N+1] are the redo list the fused kernels use
  *                       for patches whose quotients need CUDA's division slow path
- *                       (re-evaluated exactly before returning) and status[2N+2] the redo
- *                       pass's CTA counter; the redo pass leaves both at zero, so a step
- *                       loop needs no memset (zero_status = 0).
+ *                       (re-evaluated exactly before returning); status[2N+2 .. 2N+4] are
+ *                       CTA counters and a mark of the CFL tail (csrc/fvb_tail.cuh).  The
+ *                       kernels leave all of them at zero, so a step loop needs no memset
+ *                       (zero_status = 0).
  * Asynchronous on `stream`.  Returns FVB_OK or FVB_ERR_CONTRACT / FVB_ERR_CUDA. */
 int fvb_update(const fvb_spec* spec, const double* qin, double* qout, const double* cell_size,
                const double* dt, double* max_eig, uint32_t* status, int kernel, int zero_status,
@@ -100,9 +101,9 @@ int fvb_update_cfl(const fvb_spec* spec, const double* qin, double* qout, const 
                    double* dt, double* max_eig, uint32_t* status, int kernel, double cfl, double dx,
                    double* gmax, double* dt_scalar, int set_dt, void* stream);
 
-/* Number of uint32 status words fvb_update needs for n patches (2n + 3: flag,
+/* Number of uint32 status words fvb_update needs for n patches (2n + 5: flag,
  * redo count, redo list -- sized 2n for kernels that may queue a patch twice --
- * and the redo pass's CTA counter). */
+ * two CTA counters and the CFL-tail mark). */
 size_t fvb_status_words(int64_t n_patches);
 
 /* Same step from HOST arrays (the reference's calling convention, numpy

@@ -31,6 +31,7 @@
 #include "fvb_exact.cuh"
 #include "fvb_kernels.h"
 #include "fvb_layout.cuh"
+#include "fvb_tail.cuh"
 #include "fvb_tma.cuh"
 
 namespace fvb {
@@ -124,7 +125,7 @@ template <int L>
 __global__ void __launch_bounds__(NTHREADS, FVB3D_HALF_MINB)
 fused3d_half_kernel(const double* __restrict__ qin, double* __restrict__ qout, const double* __restrict__ cell_size,
                     const double* __restrict__ dtv, double* __restrict__ max_eig, unsigned* __restrict__ status,
-                    int64_t n, Closure cl) {
+                    int64_t n, Closure cl, CflTail tail) {
   extern __shared__ __align__(128) double sm[];
   double* ring = sm + OFF_RING;
   double* ysb = sm + OFF_YS;
@@ -394,6 +395,7 @@ fused3d_half_kernel(const double* __restrict__ qin, double* __restrict__ qout, c
   }
 
   if (producer) bulk_wait_all0();
+  fused_kernel_tail(tail, max_eig, status, n, producer);   // fvb_update_cfl: the step's max / dt
 }
 
 template <int L>
@@ -410,7 +412,8 @@ cudaError_t launch_impl(const FvbArgs& a, cudaStream_t st) {
   int64_t grid = (int64_t)sms * per_sm;
   if (grid > a.n) grid = a.n;
   const Closure cl{a.gamma, a.gamma - 1.0};
-  kfn<<<(unsigned)grid, NTHREADS, BYTES, st>>>(a.qin, a.qout, a.cell_size, a.dt, a.max_eig, a.status, a.n, cl);
+  const CflTail tail{a.gmax, a.cfl, a.dx, a.dt_scalar, a.dt_patches, a.tail_dt};
+  kfn<<<(unsigned)grid, NTHREADS, BYTES, st>>>(a.qin, a.qout, a.cell_size, a.dt, a.max_eig, a.status, a.n, cl, tail);
   return cudaGetLastError();
 }
 

@@ -105,11 +105,11 @@ class CflStepper:
         """One step: fvb_update_cfl (update + redo pass + local max, and on one GPU the dt in
         the same launches), then on N GPUs the all-reduce and fvb_set_dt."""
         torch = _torch()
+        st = stream   # None: torch's current stream (the capture stream inside a graph capture)
         if not self._multi():
-            self.db.update_cfl(self.cfl, self.dx, self.gmax, self.dt_scalar, kernel=self.kernel,
-                               stream=stream if stream is not None else self.stream, mode=self.mode)
+            self.db.update_cfl(self.cfl, self.dx, self.gmax, self.dt_scalar, kernel=self.kernel, stream=st,
+                               mode=self.mode)
             return
-        st = stream if stream is not None else self.stream
         self.db.update_cfl(self.cfl, self.dx, self.gmax, None, kernel=self.kernel, stream=st, mode=self.mode)
         allreduce_max_(self.gmax, self.group)
         _lib.check(_lib.load().fvb_set_dt(_vp(self.gmax), self.cfl, self.dx, _vp(self.dt_scalar), _vp(self.db.dt),
