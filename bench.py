@@ -328,7 +328,8 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=8)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-exact-leg", action="store_true")
-    ap.add_argument("--no-graph", action="store_true")
+    ap.add_argument("--graph", action="store_true",
+                    help="replay the timed steps from CUDA graphs (per-launch events then sit inside the graph)")
     ap.add_argument("--scaling", default="weak", choices=["weak", "strong"])
     ap.add_argument("--patches", type=int, default=None, help="override the patches per GPU (overhead studies)")
     args = ap.parse_args()
@@ -386,18 +387,19 @@ def main():
     kernel_name = fdev.selected_kernel(dim, p, n, gamma, args.layout) if args.kernel == "auto" else args.kernel
 
     def run_mode(mode, steps, warmup, clocks_ok):
-        """(total ms of `steps` graph-replayed steps, mean update-launch ms, redo count seen)."""
+        """(total ms of `steps` steps, mean update-launch ms).  Eager launches by default: every
+        step's update (fused kernel + its redo pass + the CFL tail) is bracketed by CUDA events
+        on the launching stream; --graph replays m-step CUDA graphs with the events inside."""
         stepper = driver.CflStepper(db, cfl=0.4, dx=1.0 / p, kernel=args.kernel, stream=stream, mode=mode,
-                                    graph=not args.no_graph)
+                                    graph=args.graph)
         stepper.prepass()
         torch.cuda.synchronize()
         if db.nonphysical():
             raise RuntimeError("synthetic input is not admissible")
-        # the timed steps: m-step CUDA graphs (m divides K), each step's update launch
-        # (fused kernel + its redo pass) bracketed by timing events inside the graph
+        # the timed steps (m divides K): the last m steps' update launches are read back
         m = max(d for d in range(1, min(steps, 32) + 1) if steps % d == 0)
         graph = None
-        if args.no_graph:
+        if not args.graph:
             ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(m)]
         else:
             graph, ev = stepper.make_graph(m, timing=True)
@@ -413,11 +415,8 @@ def main():
             if graph is not None:
                 graph.replay()
                 continue
-            for a, b in ev:
-                a.record(stream)
-                db.update(kernel=args.kernel, stream=stream, zero_status=False, mode=mode)
-                b.record(stream)
-                stepper.reduce_dt()
+            for pair in ev:
+                stepper.step(events=pair)   # the step's update launches bracketed by the pair
         t1.record(stream)
         torch.cuda.synchronize()
         if world > 1:
@@ -542,7 +541,7 @@ def main():
                        "mode": MODE_NOTE[args.mode],
                        "step": "CflStepper: fvb_update_cfl (update, redo pass with the max-reduce/dt) "
                                "(+ NCCL MAX all-reduce + set_dt)"
-                               + ("" if args.no_graph else ", CUDA-graph replay"),
+                               + (", CUDA-graph replay" if args.graph else ""),
                        "parallelism": f"patch shards x{world}, NCCL MAX all-reduce of the wave speed",
                        "l2": f"inputs {n * spec.haloed_volumes * spec.unknowns * 8 / 1e6:.0f} MB vs 126 MB L2; "
                              "no flush"},

@@ -101,16 +101,24 @@ class CflStepper:
         self.db.max_eig_prepass(stream=self.stream)
         self.reduce_dt()
 
-    def _enqueue(self, stream) -> None:
+    def _enqueue(self, stream, events=None) -> None:
         """One step: fvb_update_cfl (update + redo pass + local max, and on one GPU the dt in
-        the same launches), then on N GPUs the all-reduce and fvb_set_dt."""
+        the same launches), then on N GPUs the all-reduce and fvb_set_dt.  events = (start,
+        end) CUDA events recorded around the update launches only."""
         torch = _torch()
         st = stream   # None: torch's current stream (the capture stream inside a graph capture)
+        rec = torch.cuda.current_stream() if st is None else st
+        if events is not None:
+            events[0].record(rec)
         if not self._multi():
             self.db.update_cfl(self.cfl, self.dx, self.gmax, self.dt_scalar, kernel=self.kernel, stream=st,
                                mode=self.mode)
+            if events is not None:
+                events[1].record(rec)
             return
         self.db.update_cfl(self.cfl, self.dx, self.gmax, None, kernel=self.kernel, stream=st, mode=self.mode)
+        if events is not None:
+            events[1].record(rec)
         allreduce_max_(self.gmax, self.group)
         _lib.check(_lib.load().fvb_set_dt(_vp(self.gmax), self.cfl, self.dx, _vp(self.dt_scalar), _vp(self.db.dt),
                                           self.db.n_patches, _stream_handle(torch, st)), "fvb_set_dt")
@@ -136,10 +144,11 @@ class CflStepper:
                     events[k][1].record()
         return g, events
 
-    def step(self) -> None:
-        """update -> local max -> (all-reduce) -> dt, enqueued on the stream (or replayed)."""
+    def step(self, events=None) -> None:
+        """update -> local max -> (all-reduce) -> dt, enqueued on the stream (or replayed).
+        events: (start, end) around the update launches (eager steps only)."""
         if not self.use_graph:
-            self._enqueue(self.stream)
+            self._enqueue(self.stream, events)
             return
         torch = _torch()
         if self._graph is None:
@@ -192,7 +201,7 @@ class SimulationResult:
 
 def run_simulation(db: DeviceBatch, grid_shape, steps: int, cfl: float = 0.4, periodic: bool = True,
                    kernel="auto", dx: float | None = None, graph: bool | None = None,
-                   direct: bool | None = None) -> SimulationResult:
+                   direct: bool | None = None, diagnose: bool = True) -> SimulationResult:
     """Device-resident time loop on one GPU.
 
     db.QOut holds the initial interior field of a logical uniform patch grid
@@ -210,7 +219,14 @@ def run_simulation(db: DeviceBatch, grid_shape, steps: int, cfl: float = 0.4, pe
     graph and replays it: the step writes its history entries through a device
     step counter, so every replay is the same graph.  Results are bit-identical
     to the eager loop (graph=False), which is also the fallback when capture is
-    unavailable.  The step is GPU-bound (the host enqueues ahead), so the graph
+    unavailable.
+
+    Errors: a non-physical state raises NonPhysicalStateError with the
+    first failing step and -- with diagnose=True (the default, at the cost of one
+    device copy of the initial field) -- its patch and haloed volume, found by
+    replaying the run bit-identically up to that step and running the locator on its
+    input; a step whose global maximum wave speed is <= 0 (dt = cfl*dx/0) raises
+    TimeStepUnderflowError.  The step is GPU-bound (the host enqueues ahead), so the graph
     saves ~1 % per step against a ~3 ms capture: the default (None) replays a
     graph for runs of 64 steps or more.
     """
@@ -226,6 +242,7 @@ def run_simulation(db: DeviceBatch, grid_shape, steps: int, cfl: float = 0.4, pe
     flag_h = torch.zeros(max(steps, 1), dtype=torch.int32, device=dev)
     scratch = db.totals_scratch()
 
+    init = db.QOut.clone() if diagnose and steps > 0 else None   # replayed on the error path only
     db.halo_project_totals(grid_shape, periodic, tot_h[0], scratch)
     db.status.zero_()
     stepper = CflStepper(db, cfl=cfl, dx=dx, kernel=kernel)
@@ -300,17 +317,64 @@ def run_simulation(db: DeviceBatch, grid_shape, steps: int, cfl: float = 0.4, pe
         for _ in range(steps):
             step_body()
 
-    flags = flag_h.cpu().numpy()[:steps]
-    bad = np.flatnonzero(flags)
-    if bad.size:
-        from .errors import NonPhysicalStateError
-        raise NonPhysicalStateError("non-physical state during run_simulation", step=int(bad[0]))
+    gm = gmax_h.cpu().numpy()
+    kind, step = _first_failure(flag_h.cpu().numpy()[:steps], gm[:steps])
+    if kind == "nonphysical" and init is not None:
+        _raise_located(db, init, grid_shape, step, cfl, periodic, kernel, dx)
+    _raise_failure(kind, step, gm)
     res = SimulationResult(db.spec.dimensions)
     res.dt = [float(v) for v in dt_h.cpu().numpy()[:steps]]
     res.t = [0.0] + [float(v) for v in np.cumsum(res.dt)]
     res.max_eigenvalue = [float(v) for v in gmax_h.cpu().numpy()]
     res.totals = list(tot_h.cpu().numpy())
     return res
+
+
+def _first_failure(flags, gmax_used):
+    """(kind, step) of the first failing step, or (None, None).  Step k advances by the dt
+    set from gmax_used[k] (an underflow there comes first), then its update raises the
+    non-physical flag."""
+    import numpy as np
+
+    under = np.flatnonzero(gmax_used <= 0.0)
+    bad = np.flatnonzero(flags)
+    ku = int(under[0]) if under.size else None
+    kb = int(bad[0]) if bad.size else None
+    if ku is not None and (kb is None or ku <= kb):
+        return "underflow", ku
+    if kb is not None:
+        return "nonphysical", kb
+    return None, None
+
+
+def _raise_failure(kind, step, gm) -> None:
+    if kind == "underflow":
+        from .errors import TimeStepUnderflowError
+        raise TimeStepUnderflowError(f"dt underflow: global max eigenvalue {float(gm[step])!r} <= 0", step=step)
+    if kind == "nonphysical":
+        from .errors import NonPhysicalStateError
+        raise NonPhysicalStateError("non-physical state during run_simulation", step=step)
+
+
+def _raise_located(db, init, grid_shape, step, cfl, periodic, kernel, dx) -> None:
+    """Replay the run (bit-identical, eager) from the saved initial field up to `step`, then
+    locate the first inadmissible volume of that step's input (patch-wise order) and raise
+    with step, patch and haloed volume."""
+    from .errors import NonPhysicalStateError
+    from .kernel import Ordering, box_volume, first_error
+
+    db.QOut.copy_(init)
+    if step > 0:
+        run_simulation(db, grid_shape, step, cfl=cfl, periodic=periodic, kernel=kernel, dx=dx, graph=False,
+                       diagnose=False)
+    else:
+        db.halo_project(grid_shape, periodic)
+    hit = first_error(db.locate(), Ordering.PATCH_WISE, 1)
+    if hit is None:  # pragma: no cover - the flag and the locator disagree
+        raise NonPhysicalStateError("non-physical state during run_simulation", step=step)
+    msg, patch, box, lin = hit
+    d, p = db.spec.dimensions, db.spec.volumes_per_axis
+    raise NonPhysicalStateError(msg, patch=patch, volume=box_volume(d, p, box, lin), step=step)
 
 
 # --- sharded grid: ghost-layer exchange + windowed halo projection (multi-GPU run_simulation) ---------
@@ -505,10 +569,8 @@ def run_simulation_sharded(sg: ShardedGrid, steps: int, cfl: float = 0.4, kernel
     flags = flag_h.clone()
     if multi:
         dist.all_reduce(flags, op=dist.ReduceOp.MAX, group=sg.group)
-    bad = np.flatnonzero(flags.cpu().numpy()[:steps])
-    if bad.size:
-        from .errors import NonPhysicalStateError
-        raise NonPhysicalStateError("non-physical state during run_simulation", step=int(bad[0]))
+    gm = gmax_h.cpu().numpy()   # global after the all-reduce: the same on every rank
+    _raise_failure(*_first_failure(flags.cpu().numpy()[:steps], gm[:steps]), gm)
     res = SimulationResult(db.spec.dimensions)
     res.dt = [float(v) for v in dt_h.cpu().numpy()[:steps]]
     res.t = [0.0] + [float(v) for v in np.cumsum(res.dt)]

@@ -2,11 +2,12 @@
 
 The north star's parity bar is a relative tolerance of 1e-12 in fp64
 (BASELINE.json); SPEC.md:374 / :378 define it as the relative max-norm per
-unknown.  Fast mode must meet that bar for QOut (it measures ~1e-16), keep
-max_eigenvalue bit-exact, keep the reference's error semantics, and keep the
-exact invariants the face-shared flux makes possible: a constant state and
-dt = 0 reproduce QIn's interior bit for bit, and the update conserves the
-totals over a periodic grid to rounding.
+unknown.  Fast mode must meet that bar for QOut (it measures ~1e-16) and for
+max_eigenvalue (a few ulp: the sound speed comes from the one-pass closure),
+keep the reference's error semantics, and keep the exact invariants the
+face-shared flux makes possible: a constant state and dt = 0 reproduce QIn's
+interior bit for bit, and the update conserves the totals over a periodic grid
+to rounding.
 """
 
 import json
@@ -43,6 +44,21 @@ def rel_maxnorm(a, b, s):
     return float(np.max(num / den))
 
 
+def assert_max_eig_close(got, ref, what="max_eig"):
+    """Wave speeds within 1e-12 relative (and ~1e-15 by design); NaN where the reference has NaN."""
+    got, ref = np.asarray(got, dtype=np.float64), np.asarray(ref, dtype=np.float64)
+    nan = np.isnan(ref)
+    assert np.array_equal(np.isnan(got), nan), what
+    g, r = got[~nan], ref[~nan]
+    inf = np.isinf(r)
+    assert np.array_equal(g[inf], r[inf]), what
+    g, r = g[~inf], r[~inf]
+    if r.size:
+        rel = np.max(np.abs(g - r) / np.maximum(np.abs(r), np.finfo(np.float64).tiny))
+        assert rel <= TOL, (what, rel)
+        assert rel < 1e-14, (what, "far above the few-ulp design accuracy", rel)
+
+
 def _batch(n, seed, p=16, vary=True):
     b = mesh.make_patch_batch(mesh.PatchSpec(3, p, 5), n)
     b.QIn[...] = oracle.synthetic_qin(3, p, n, seed=seed)
@@ -72,7 +88,7 @@ def test_fast_golden(case):
     b.max_eigenvalue[...] = 0.0
     update_patch_batch(b, pde.make_euler_pde(3, pde.EulerParameters(case["gamma"])), PW, mode="fast")
     assert rel_maxnorm(b.QOut, gold.QOut, 5) <= TOL, case["name"]
-    assert_bits_equal(b.max_eigenvalue, gold.max_eigenvalue, case["name"] + " max_eig")
+    assert_max_eig_close(b.max_eigenvalue, gold.max_eigenvalue, case["name"] + " max_eig")
 
 
 @pytest.mark.parametrize("n,seed", [(1, 3), (7, 4), (300, 5), (1000, 6)])
@@ -85,7 +101,7 @@ def test_fast_random_vs_oracle(n, seed):
     err = rel_maxnorm(out.QOut, ref_q, 5)
     assert err <= TOL, err
     assert err < 1e-14, f"fast mode drifted far above its ~1e-16 design accuracy: {err}"
-    assert_bits_equal(out.max_eigenvalue, ref_l, "max_eig")
+    assert_max_eig_close(out.max_eigenvalue, ref_l)
 
 
 def test_fast_full_size_c3():
@@ -96,7 +112,7 @@ def test_fast_full_size_c3():
     b2 = b.copy()
     update_patch_batch(b2, pde.make_euler_pde(3), variant_from_labels("batched", "soa", "par"), mode="fast")
     assert rel_maxnorm(b2.QOut, ref_q, 5) <= TOL
-    assert_bits_equal(b2.max_eigenvalue, ref_l, "max_eig")
+    assert_max_eig_close(b2.max_eigenvalue, ref_l)
 
 
 def test_fast_constant_state_and_dt0_bitwise():
@@ -147,7 +163,7 @@ def test_fast_signed_zero_and_rest(dt_value):
     db, out = _fast_device(b)
     assert not db.nonphysical()
     assert rel_maxnorm(out.QOut, ref_q, 5) <= TOL
-    assert_bits_equal(out.max_eigenvalue, ref_l, "max_eig")
+    assert_max_eig_close(out.max_eigenvalue, ref_l)
 
 
 def test_fast_extreme_values_take_the_exact_path():
@@ -169,7 +185,7 @@ def test_fast_extreme_values_take_the_exact_path():
     r = np.where(fin, ref_q, 0.0)
     for k in range(n):   # per patch: the extreme patches must not set the others' scale
         assert rel_maxnorm(a[k], r[k], 5) <= TOL, k
-    assert_bits_equal(out.max_eigenvalue, ref_l, "max_eig")
+    assert_max_eig_close(out.max_eigenvalue, ref_l)
 
 
 @pytest.mark.parametrize("case", [c for c in MANIFEST["error_cases"] if c["dim"] == 3], ids=lambda c: c["name"])
