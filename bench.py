@@ -396,10 +396,12 @@ def main():
         torch.cuda.synchronize()
         if db.nonphysical():
             raise RuntimeError("synthetic input is not admissible")
-        # the timed steps (m divides K): the last m steps' update launches are read back
+        # the timed steps: eager -- every step's update launches bracketed by their own event
+        # pair; --graph -- m-step graphs (m divides K), the last m steps' pairs read back
         m = max(d for d in range(1, min(steps, 32) + 1) if steps % d == 0)
         graph = None
         if not args.graph:
+            m = steps
             ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(m)]
         else:
             graph, ev = stepper.make_graph(m, timing=True)
@@ -422,7 +424,7 @@ def main():
         if world > 1:
             dist.barrier()
         total = t0.elapsed_time(t1)
-        kern = statistics.mean(a.elapsed_time(b) for a, b in ev)   # the last m steps of the timed region
+        kern = statistics.median(a.elapsed_time(b) for a, b in ev)   # per-launch duration (median)
         if world > 1:
             t = torch.tensor([total, kern], dtype=torch.float64, device="cuda")
             dist.all_reduce(t, op=dist.ReduceOp.MAX)

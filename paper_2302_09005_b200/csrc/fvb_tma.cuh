@@ -158,6 +158,10 @@ __device__ __forceinline__ void tma_store_1d(void* dst, const void* src, uint32_
                "r"(bytes)
                : "memory");
 }
+// Bulk prefetch of a global range into L2 (no shared memory, no completion tracking).
+__device__ __forceinline__ void prefetch_l2(const void* src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
+}
 __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void bulk_wait_read0() {
   asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
