@@ -359,3 +359,36 @@ def test_cfl_stepper_graph_equals_eager(mode, explicit_stream):
     assert_bits_equal(res[0][0], res[1][0], "QOut")
     assert_bits_equal(res[0][1], res[1][1], "max_eig")
     assert res[0][2] == res[1][2]
+
+
+def test_run_simulation_dt_underflow_raises():
+    """a zero global wave speed with a nonzero field (here rho = 1, j = 0, E = 0,
+    so p = c = 0) cannot set dt = cfl*dx/max -- run_simulation raises instead of stepping with
+    an infinite dt."""
+    from paper_2302_09005_b200.errors import TimeStepUnderflowError
+
+    dim, p, grid = 2, 8, (2, 2)
+    n = int(np.prod(grid))
+    field = np.tile(np.array([1.0, 0.0, 0.0, 0.0]), (n, p ** dim))
+    db = _db_with_field(dim, p, grid, field)
+    with pytest.raises(TimeStepUnderflowError) as ei:
+        driver.run_simulation(db, grid, steps=3, cfl=0.4, periodic=True)
+    assert ei.value.step == 0
+    assert "step=0" in str(ei.value)
+
+
+@pytest.mark.parametrize("graph", [False, True])
+def test_run_simulation_nonphysical_is_located(graph):
+    """A non-physical volume aborts the run with the step, patch and haloed volume (SPEC.md:451,
+    the reference's NonPhysicalStateError fields), found by replaying the run to that step."""
+    from paper_2302_09005_b200.errors import NonPhysicalStateError
+
+    dim, p, grid = 2, 16, (3, 3)
+    n = int(np.prod(grid))
+    state = pde.euler_state(1.0, [0.2, 0.1], 1.0)
+    field = np.tile(state, (n, p ** dim)).reshape(n, p, p, 4)
+    field[4, 7, 5, 0] = -1.0          # patch 4, interior cell (x=5, y=7): rho < 0
+    db = _db_with_field(dim, p, grid, field.reshape(n, -1))
+    with pytest.raises(NonPhysicalStateError) as ei:
+        driver.run_simulation(db, grid, steps=70, cfl=0.4, periodic=True, graph=graph)
+    assert (ei.value.step, ei.value.patch, ei.value.volume) == (0, 4, (6, 8)), str(ei.value)
