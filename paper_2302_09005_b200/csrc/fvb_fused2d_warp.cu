@@ -29,6 +29,7 @@
 #include <cuda_runtime.h>
 
 #include "fvb_exact.cuh"
+#include "fvb_fast.cuh"
 #include "fvb_kernels.h"
 #include "fvb_layout.cuh"
 #include "fvb_tma.cuh"
@@ -101,7 +102,11 @@ __device__ __forceinline__ bool inv_ok(double inv) {
   return inv == 0.0 || (e >= 2u && e < 0x7ffu);
 }
 
-template <int P>
+// FAST (mode "fast", fvb_fast.cuh): one closure per volume with FMA contraction, face
+// fluxes shared by the two cells of a face (the y face is carried down the march, both x
+// faces are formed by the lane from its own and its neighbours' reconstructions), QOut
+// within ~1e-16 relative of the reference instead of bit-exact.
+template <int P, bool FAST = false>
 __global__ void __launch_bounds__(WPC * 32, 4)
 fused2d_warp_kernel(const double* __restrict__ qin, double* __restrict__ qout, const double* __restrict__ cell_size,
                     const double* __restrict__ dtv, double* __restrict__ max_eig, unsigned* __restrict__ status,
@@ -215,8 +220,9 @@ fused2d_warp_kernel(const double* __restrict__ qin, double* __restrict__ qout, c
     double oq[S], olx = 0.0, ofx[3] = {0.0, 0.0, 0.0};
     Side<2> yprev;
     double tp[S], favg[S];
+    double gyl[S];   // FAST: the lower y face of row hy-1
 #pragma unroll
-    for (int u = 0; u < S; ++u) { oq[u] = 0.0; tp[u] = 0.0; favg[u] = 0.0; }
+    for (int u = 0; u < S; ++u) { oq[u] = 0.0; tp[u] = 0.0; favg[u] = 0.0; gyl[u] = 0.0; }
     yprev.lam = 0.0;
 #pragma unroll
     for (int k = 0; k < 3; ++k) yprev.f[k] = 0.0;
@@ -241,8 +247,13 @@ fused2d_warp_kernel(const double* __restrict__ qin, double* __restrict__ qout, c
           double qh[S];
           lds_q(hst + (side ? E - 1 : 0) * S, qh);
           Side<2> sh;
-          bool ok;
-          closure_one_ranged<2>(qh, cl, 0, sh, ok);
+          bool ok = true;
+          if constexpr (FAST) {
+            const fast::Rpc w = fast::closure<2>(qh, cl, ok);
+            sh.lam = fast::recon<2>(qh, w, 0, sh.f);
+          } else {
+            closure_one_ranged<2>(qh, cl, 0, sh, ok);
+          }
           const int idx = (((hy + dr - 1) & (HXR - 1)) * 2 + side) * 2 + hps;
           hxs[0 * HXC + idx] = sh.lam;
 #pragma unroll
@@ -260,8 +271,14 @@ fused2d_warp_kernel(const double* __restrict__ qin, double* __restrict__ qout, c
       double nlx = 0.0, nfx[3] = {0.0, 0.0, 0.0};
       if (hy >= 1 && hy <= P) {
         Side<2> sd2[2];
-        bool ok;
-        closure_all_ranged<2>(q, cl, sd2, ok);
+        bool ok = true;
+        if constexpr (FAST) {
+          const fast::Rpc w = fast::closure<2>(q, cl, ok);
+          sd2[0].lam = fast::recon<2>(q, w, 0, sd2[0].f);
+          sd2[1].lam = fast::recon<2>(q, w, 1, sd2[1].f);
+        } else {
+          closure_all_ranged<2>(q, cl, sd2, ok);
+        }
         if (HL && hlane) hslow = hslow | !ok;   // x-face halo volume: gated like the reference's face box
         else slow = slow | !ok;
         const unsigned long long a = (unsigned long long)__double_as_longlong(sd2[0].lam);
@@ -277,8 +294,13 @@ fused2d_warp_kernel(const double* __restrict__ qin, double* __restrict__ qout, c
         for (int k = 0; k < 3; ++k) nfx[k] = sd2[0].f[k];
         ycur = sd2[1];
       } else {   // y-face halo rows: only their y-side data
-        bool ok;
-        closure_one_ranged<2>(q, cl, 1, ycur, ok);
+        bool ok = true;
+        if constexpr (FAST) {
+          const fast::Rpc w = fast::closure<2>(q, cl, ok);
+          ycur.lam = fast::recon<2>(q, w, 1, ycur.f);
+        } else {
+          closure_one_ranged<2>(q, cl, 1, ycur, ok);
+        }
         slow = slow | !ok;
       }
       // No __syncwarp here: the update below reads only data published in earlier
@@ -286,7 +308,46 @@ fused2d_warp_kernel(const double* __restrict__ qin, double* __restrict__ qout, c
       // update of row hy-1 form one block the scheduler interleaves; the syncwarp at
       // the end of the step publishes row hy's x-side data and this step's halo batch.
 
-      if (hy == 1) {
+      if (FAST && hy == 1) {
+        fast::face<2>(gyl, 1, oq, yprev.lam, yprev.f, q, ycur.lam, ycur.f);   // face (0 | 1)
+      } else if (FAST && hy >= 2) {
+        // ---- fast update of this lane's cell of row hy-1: both x faces from the lane's and
+        // its neighbours' reconstructions, the y faces carried / formed here ----
+        const double* xr = xsb + ((hy - 1) & 1) * XSD;
+        const double* hr = hxs + ((hy - 2) & (HXR - 1)) * 4 + ps;
+        const double* ml = lh ? hr : xr + (HL && l == 0 ? 0 : l - LST);
+        const double* mr = rh ? hr + 2 : xr + (HL && l == 31 ? 31 : l + LST);
+        double qn[S], fn[3], gx_lo[S], gx_hi[S], gy_hi[S], val[S];
+        lds_q(stp + left, qn);
+#pragma unroll
+        for (int k = 0; k < 3; ++k) fn[k] = ml[(k + 1) * lcs];
+        fast::face<2>(gx_lo, 0, qn, ml[0], fn, oq, olx, ofx);
+        lds_q(stp + right, qn);
+#pragma unroll
+        for (int k = 0; k < 3; ++k) fn[k] = mr[(k + 1) * rcs];
+        fast::face<2>(gx_hi, 0, oq, olx, ofx, qn, mr[0], fn);
+        fast::face<2>(gy_hi, 1, oq, yprev.lam, yprev.f, q, ycur.lam, ycur.f);
+#pragma unroll
+        for (int u = 0; u < S; ++u) {
+          val[u] = __fma_rn(half_inv, dsub(dadd(gx_lo[u], gyl[u]), dadd(gx_hi[u], gy_hi[u])), oq[u]);
+          gyl[u] = gy_hi[u];
+        }
+        const int z = hy - 2;
+        if (!(z & 1)) {
+          if (l == 0) bulk_wait_read<0>();
+          __syncwarp();
+        }
+        if (act) sts_q(outb + ps * OFFO + (z & 1) * OUTR + x * S, val);
+        if ((z & 1) || ((P & 1) && z == P - 1)) {
+          const int z0 = z & ~1;
+          fence_proxy_async();
+          __syncwarp();
+          if (l == 0) {
+            tma_store_3d(&omap, out_haloed ? S : 0, z0 + out_haloed, (int)pa, outb);
+            bulk_commit();
+          }
+        }
+      } else if (hy == 1) {
         // the face (0 | 1): minus face of the first interior row
         const double cy = dmul(half_inv, speed_max(ycur.lam, yprev.lam));
 #pragma unroll
@@ -433,9 +494,9 @@ cudaError_t make_qout_map(const FvbArgs& a, CUtensorMap* tm) {
   return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
 }
 
-template <int P>
+template <int P, bool FAST = false>
 cudaError_t launch(const FvbArgs& a, cudaStream_t st) {
-  auto kfn = fused2d_warp_kernel<P>;
+  auto kfn = fused2d_warp_kernel<P, FAST>;
   constexpr size_t BYTES = bytes_of<P>();
   cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)BYTES);
   if (e != cudaSuccess) return e;
@@ -478,4 +539,12 @@ cudaError_t fvb_launch_fused2d16_warp(const FvbArgs& a, cudaStream_t st) {
     default:
       return cudaErrorInvalidValue;
   }
+}
+
+// mode "fast" (fvb_fast.cuh): 2D p = 16 AoS (BASELINE configs[1]); other shapes run the exact kernels
+bool fvb_fast2d_supported(int dim, int p, int layout) { return dim == 2 && p == 16 && layout == fvb::kAoS; }
+
+cudaError_t fvb_launch_fast2d16(const FvbArgs& a, cudaStream_t st) {
+  if (a.n <= 0) return cudaSuccess;
+  return fvb::f2w::launch<16, true>(a, st);
 }

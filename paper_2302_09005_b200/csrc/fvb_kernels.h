@@ -40,6 +40,8 @@ cudaError_t fvb_launch_fused2d16_warp(const FvbArgs& a, cudaStream_t st);
 bool fvb_fused2d_warp_supported(int p);
 bool fvb_fast3d_supported(int dim, int p, int layout);
 cudaError_t fvb_launch_fast3d16(const FvbArgs& a, cudaStream_t st);
+bool fvb_fast2d_supported(int dim, int p, int layout);
+cudaError_t fvb_launch_fast2d16(const FvbArgs& a, cudaStream_t st);
 cudaError_t fvb_launch_redo(const FvbArgs& a, cudaStream_t st);
 bool fvb_fused16_supported(int dim, int p, int layout);
 bool fvb_small3d_supported(int dim, int p, int layout);

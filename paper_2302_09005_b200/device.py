@@ -51,7 +51,7 @@ MODES = {"exact": 0, "fast": 0x100}   # FVB_MODE_FAST (include/fvb200.h)
 
 
 def kernel_id(kernel, mode: str = "exact") -> int:
-    """C-ABI kernel selector; mode "fast" ORs in FVB_MODE_FAST (1e-12 relative, exact max_eig)."""
+    """C-ABI kernel selector; mode "fast" ORs in FVB_MODE_FAST (1e-12 relative parity)."""
     if mode not in MODES:
         raise ContractViolationError(f"unknown mode {mode!r} (expected 'exact' or 'fast')")
     if isinstance(kernel, int):

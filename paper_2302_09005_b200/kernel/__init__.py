@@ -212,9 +212,11 @@ def update_patch_batch(batch: PatchBatch, pde: PdeDefinition, variant: KernelVar
     arguments select the CUDA device, the kernel ("auto" | "fused" |
     "generic"), an explicit gamma, the host pipeline chunk size and the
     arithmetic mode: "exact" (default; bit-identical to the reference) or
-    "fast" (QOut within 1e-12 relative max-norm per unknown -- the north
-    star's parity bar -- with max_eigenvalue still bit-exact; see
-    csrc/fvb_fast3d.cu).  Shapes without a fast kernel run the exact one.
+    "fast" (QOut and max_eigenvalue within 1e-12 relative per unknown -- the
+    north star's parity bar; measured ~1e-16 -- with face-shared fluxes and one
+    closure per volume: csrc/fvb_fast3d.cu for 3D p = 16, the FAST warp kernel
+    of csrc/fvb_fused2d_warp.cu for 2D p = 16).  Shapes without a fast kernel
+    run the exact one.
     """
     if batch.n_patches == 0:
         return
