@@ -123,6 +123,8 @@ int update_impl(const fvb_spec* spec, const double* qin, double* qout, const dou
   } else if (fast && fvb_fast3d_supported(spec->dim, spec->p, spec->layout)) {
     e = fvb_launch_fast3d16(a, st);
     if (e == cudaSuccess) e = fvb_launch_redo(a, st);   // exact re-evaluation of queued patches
+  } else if (fast && fvb_fast_small3d_supported(spec->dim, spec->p, spec->layout)) {
+    e = fvb_launch_fast_small3d(a, st);
   } else if (fast && fvb_fast2d_supported(spec->dim, spec->p, spec->layout)) {
     e = fvb_launch_fast2d16(a, st);
     if (e == cudaSuccess) e = fvb_launch_redo(a, st);

@@ -41,6 +41,8 @@ bool fvb_fused2d_warp_supported(int p);
 bool fvb_fast3d_supported(int dim, int p, int layout);
 cudaError_t fvb_launch_fast3d16(const FvbArgs& a, cudaStream_t st);
 bool fvb_fast2d_supported(int dim, int p, int layout);
+bool fvb_fast_small3d_supported(int dim, int p, int layout);
+cudaError_t fvb_launch_fast_small3d(const FvbArgs& a, cudaStream_t st);   // includes its redo pass
 cudaError_t fvb_launch_fast2d16(const FvbArgs& a, cudaStream_t st);
 cudaError_t fvb_launch_redo(const FvbArgs& a, cudaStream_t st);
 bool fvb_fused16_supported(int dim, int p, int layout);

@@ -17,6 +17,7 @@
 #include <cuda_runtime.h>
 
 #include "fvb_exact.cuh"
+#include "fvb_fast.cuh"
 #include <cstring>
 
 #include "fvb_kernels.h"
@@ -109,7 +110,10 @@ constexpr bool TOUT = FVB_SMALL3D_TOUT != 0;
 #define FVB_SMALL3D_REMAP 1
 #endif
 
-template <int P>
+// FAST (mode "fast", fvb_fast.cuh): the same staging and side-data records, filled from one
+// FMA closure per volume; phase B forms each of the cell's six faces as the shared flux G
+// (the neighbour forms the same G bit for bit), QOut within ~1e-16 relative.
+template <int P, bool FAST = false>
 __global__ void __launch_bounds__(Cfg<P>::THREADS, P == 4 ? 6 / Cfg<P>::PPC : 1)
 small3d_kernel(const double* __restrict__ qin, double* __restrict__ qout, const double* __restrict__ cell_size,
                const double* __restrict__ dtv, double* __restrict__ max_eig, unsigned* __restrict__ status,
@@ -239,8 +243,14 @@ small3d_kernel(const double* __restrict__ qin, double* __restrict__ qout, const 
       double q[S];
       load(cx + 1, cy + 1, cz + 1, q);
       Side<3> sd[3];
-      bool ok;
-      closure_all_ranged<3>(q, cl, sd, ok);
+      bool ok = true;
+      if constexpr (FAST) {
+        const fast::Rpc w = fast::closure<3>(q, cl, ok);
+#pragma unroll
+        for (int d = 0; d < 3; ++d) sd[d].lam = fast::recon<3>(q, w, d, sd[d].f);
+      } else {
+        closure_all_ranged<3>(q, cl, sd, ok);
+      }
       slow = slow | !ok;
       unsigned long long m = (unsigned long long)__double_as_longlong(sd[0].lam);
       unsigned long long v = (unsigned long long)__double_as_longlong(sd[1].lam);
@@ -265,10 +275,17 @@ small3d_kernel(const double* __restrict__ qin, double* __restrict__ qout, const 
 #pragma unroll
       for (int u = 0; u < S; ++u) qh[u] = stt[((hz * E + hy) * E + hx) * S + u];
       Side<3> sh;
-      bool okh;
-      if (nd == 0) closure_one_ranged<3>(qh, cl, 0, sh, okh);
-      else if (nd == 1) closure_one_ranged<3>(qh, cl, 1, sh, okh);
-      else closure_one_ranged<3>(qh, cl, 2, sh, okh);
+      bool okh = true;
+      if constexpr (FAST) {
+        const fast::Rpc w = fast::closure<3>(qh, cl, okh);
+        sh.lam = fast::recon<3>(qh, w, nd, sh.f);
+      } else if (nd == 0) {
+        closure_one_ranged<3>(qh, cl, 0, sh, okh);
+      } else if (nd == 1) {
+        closure_one_ranged<3>(qh, cl, 1, sh, okh);
+      } else {
+        closure_one_ranged<3>(qh, cl, 2, sh, okh);
+      }
       if (!okh) atomicOr(&slowflag[g & 1], 1u << lpt);   // rare: queue that patch for the exact pass
       put_rec<P>(sideb + lpt * C::SIDE, nd, hn, a, b, sh);
     };
@@ -317,7 +334,41 @@ small3d_kernel(const double* __restrict__ qin, double* __restrict__ qout, const 
     __syncthreads();
 
     // ---- B: face terms and update of this thread's cell ----
-    if (active) {
+    if (FAST && active) {
+      double qc[S], qn[S], val[S], slo[S], shi[S];
+      load(cx + 1, cy + 1, cz + 1, qc);
+      const int hcc[3] = {cx + 1, cy + 1, cz + 1};
+      const int ab[3][2] = {{cy, cz}, {cx, cz}, {cx, cy}};
+#pragma unroll
+      for (int nd = 0; nd < 3; ++nd) {
+        double fc[4], fn[4], G[S];
+        const double lc = side[side_at<P>(nd, 0, hcc[nd], ab[nd][0], ab[nd][1])];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) fc[k] = side[side_at<P>(nd, k + 1, hcc[nd], ab[nd][0], ab[nd][1])];
+#pragma unroll
+        for (int sh = -1; sh <= 1; sh += 2) {
+          int hq[3] = {hcc[0], hcc[1], hcc[2]};
+          hq[nd] += sh;
+          load(hq[0], hq[1], hq[2], qn);
+          const double ln = side[side_at<P>(nd, 0, hcc[nd] + sh, ab[nd][0], ab[nd][1])];
+#pragma unroll
+          for (int k = 0; k < 4; ++k) fn[k] = side[side_at<P>(nd, k + 1, hcc[nd] + sh, ab[nd][0], ab[nd][1])];
+          if (sh < 0) fast::face<3>(G, nd, qn, ln, fn, qc, lc, fc);   // lower face: neighbour below
+          else fast::face<3>(G, nd, qc, lc, fc, qn, ln, fn);          // upper face: neighbour above
+#pragma unroll
+          for (int u = 0; u < S; ++u) {
+            if (sh < 0) slo[u] = nd == 0 ? G[u] : dadd(slo[u], G[u]);
+            else shi[u] = nd == 0 ? G[u] : dadd(shi[u], G[u]);
+          }
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < S; ++u) val[u] = __fma_rn(half_inv, dsub(slo[u], shi[u]), qc[u]);
+      const int lin = TOUT_P ? (cy * P + cz) * P + cx : (cz * P + cy) * P + cx;
+#pragma unroll
+      for (int u = 0; u < S; ++u) outb[(g % C::NOB) * C::OUTN + (lp * C::IVOL + lin) * S + u] = val[u];
+      if (!ODD) fence_proxy_async();
+    } else if (active) {
       double qc[S], qn[S], val[S];
       load(cx + 1, cy + 1, cz + 1, qc);
 #pragma unroll
@@ -403,10 +454,10 @@ small3d_kernel(const double* __restrict__ qin, double* __restrict__ qout, const 
   if (tid == 0) bulk_wait_all0();
 }
 
-template <int P>
+template <int P, bool FAST = false>
 cudaError_t launch(const FvbArgs& a, cudaStream_t st) {
   using C = Cfg<P>;
-  auto kfn = small3d_kernel<P>;
+  auto kfn = small3d_kernel<P, FAST>;
   cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::BYTES);
   if (e != cudaSuccess) return e;
   int dev = 0, sms = 148;
@@ -463,6 +514,16 @@ cudaError_t fvb_launch_small3d(const FvbArgs& a, cudaStream_t st) {
     case 8: e = fvb::fs::launch<8>(a, st); break;
     default: return cudaErrorInvalidValue;
   }
+  if (e != cudaSuccess) return e;
+  return fvb_launch_redo(a, st);
+}
+
+// mode "fast" (fvb_fast.cuh): 3D p = 4 AoS (BASELINE configs[3]); other small shapes run exact
+bool fvb_fast_small3d_supported(int dim, int p, int layout) { return dim == 3 && p == 4 && layout == fvb::kAoS; }
+
+cudaError_t fvb_launch_fast_small3d(const FvbArgs& a, cudaStream_t st) {
+  if (a.n <= 0) return cudaSuccess;
+  const cudaError_t e = fvb::fs::launch<4, true>(a, st);
   if (e != cudaSuccess) return e;
   return fvb_launch_redo(a, st);
 }

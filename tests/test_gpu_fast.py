@@ -208,7 +208,7 @@ def test_fast_error_semantics(case):
 
 def test_fast_mode_other_shapes_fall_back_to_exact():
     """No fast kernel for p != 16: mode="fast" runs the exact kernels (bitwise)."""
-    for dim, p, n in [(2, 17, 40), (2, 8, 30), (3, 4, 50), (3, 7, 5)]:
+    for dim, p, n in [(2, 17, 40), (2, 8, 30), (3, 6, 20), (3, 7, 5)]:
         b = mesh.make_patch_batch(mesh.PatchSpec(dim, p, dim + 2), n)
         b.QIn[...] = oracle.synthetic_qin(dim, p, n, seed=3)
         b.dt[...] = 0.4 * (1.0 / p) / 3.4
@@ -287,3 +287,55 @@ def test_fast2d_error_semantics(case):
         with pytest.raises(NonPhysicalStateError) as ei:
             update_patch_batch(b, pd, v, mode="fast")
         assert str(ei.value) == exp["str"]
+
+
+# ---- 3D p = 4 (BASELINE configs[3]): the FAST small-patch kernel ----
+
+@pytest.mark.parametrize("n,seed", [(1, 31), (5, 32), (333, 33), (20000, 34)])
+def test_fast_small3d_random_vs_oracle(n, seed):
+    b = _batch(n, seed, p=4)
+    ref_q, ref_l, st = oracle.update(3, 4, 1.4, b.QIn, b.cell_size, b.dt)
+    assert st == 0
+    db, out = _fast_device(b)
+    assert not db.nonphysical()
+    err = rel_maxnorm(out.QOut, ref_q, 5)
+    assert err <= TOL and err < 1e-14, err
+    assert_max_eig_close(out.max_eigenvalue, ref_l)
+
+
+def test_fast_small3d_constant_state_dt0_and_conservation():
+    n = 40
+    b = mesh.make_patch_batch(mesh.PatchSpec(3, 4, 5), n)
+    q = b.qin_view()
+    rng = np.random.default_rng(35)
+    for k in range(n):
+        q[k] = pde.euler_state(rng.uniform(0.5, 2), rng.uniform(-1, 1, 3), rng.uniform(0.5, 2))
+    b.dt[...] = rng.uniform(0.0, 0.01, size=n)
+    _, out = _fast_device(b)
+    assert_bits_equal(out.QOut, b.qin_view()[:, 1:-1, 1:-1, 1:-1, :].reshape(n, -1), "constant state")
+    r = _batch(n, 36, p=4)
+    r.dt[...] = 0.0
+    _, out = _fast_device(r)
+    assert_bits_equal(out.QOut, r.qin_view()[:, 1:-1, 1:-1, 1:-1, :].reshape(n, -1), "dt = 0")
+    grid = (3, 2, 4)
+    g = _batch(24, 37, p=4, vary=False)
+    g.QOut[...] = g.qin_view()[:, 1:-1, 1:-1, 1:-1, :].reshape(24, -1)
+    mesh.halo_project(g, grid, True)
+    before = g.QOut.reshape(-1, 5).sum(axis=0)
+    _, out = _fast_device(g)
+    after = out.QOut.reshape(-1, 5).sum(axis=0)
+    scale = np.abs(g.QOut.reshape(-1, 5)).sum(axis=0)
+    assert np.all(np.abs(after - before) <= 1e-13 * scale), (after - before) / scale
+
+
+def test_fast_small3d_golden_and_errors():
+    """The reference-written 3D p = 4 cases: solution within the bar, NaN corners untouched."""
+    for case in [c for c in MANIFEST["solution_cases"] if c["p"] == 4 and c["dim"] == 3]:
+        gold = load_golden(case["file"])
+        b = gold.copy()
+        b.QOut[...] = 0.0
+        update_patch_batch(b, pde.make_euler_pde(3, pde.EulerParameters(case["gamma"])), PW, mode="fast")
+        fin = np.isfinite(gold.QOut)
+        assert np.array_equal(np.isfinite(b.QOut), fin), case["name"]
+        assert rel_maxnorm(np.where(fin, b.QOut, 0.0), np.where(fin, gold.QOut, 0.0), 5) <= TOL, case["name"]
+        assert_max_eig_close(b.max_eigenvalue, gold.max_eigenvalue, case["name"])
