@@ -278,7 +278,10 @@ small3d_kernel(const double* __restrict__ qin, double* __restrict__ qout, const 
       bool okh = true;
       if constexpr (FAST) {
         const fast::Rpc w = fast::closure<3>(qh, cl, okh);
-        sh.lam = fast::recon<3>(qh, w, nd, sh.f);
+        // constant normals (a run-time n would index qh dynamically: local memory)
+        if (nd == 0) sh.lam = fast::recon<3>(qh, w, 0, sh.f);
+        else if (nd == 1) sh.lam = fast::recon<3>(qh, w, 1, sh.f);
+        else sh.lam = fast::recon<3>(qh, w, 2, sh.f);
       } else if (nd == 0) {
         closure_one_ranged<3>(qh, cl, 0, sh, okh);
       } else if (nd == 1) {
