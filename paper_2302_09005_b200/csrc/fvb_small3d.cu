@@ -29,7 +29,7 @@ namespace fs {
 
 using namespace f16;
 
-template <int P>
+template <int P, bool FAST = false>
 struct Cfg {
   static constexpr int S = 5;
   static constexpr int E = P + 2;
@@ -49,7 +49,8 @@ struct Cfg {
   static constexpr int LINE = E * P * P;            // records of one direction: (E along n) x P x P
   static constexpr int STAGE = PPC * VOL * S;       // doubles per ring stage
   static constexpr int NST = 2;
-  static constexpr int SIDE = 3 * S * LINE;         // side data of one patch, 3 directions
+  // exact: side data of one patch, 3 directions; FAST: (r, p, c) of every haloed volume
+  static constexpr int SIDE = FAST ? VOL * 3 : 3 * S * LINE;
   static constexpr int OUTN = (PPC * IVOL * S + 15) / 16 * 16;   // staging buffers 128-byte aligned (TMA)
   static constexpr int OFF_RING = 0;
   static constexpr int OFF_SIDE = OFF_RING + NST * STAGE;
@@ -114,11 +115,11 @@ constexpr bool TOUT = FVB_SMALL3D_TOUT != 0;
 // FMA closure per volume; phase B forms each of the cell's six faces as the shared flux G
 // (the neighbour forms the same G bit for bit), QOut within ~1e-16 relative.
 template <int P, bool FAST = false>
-__global__ void __launch_bounds__(Cfg<P>::THREADS, P == 4 ? 6 / Cfg<P>::PPC : 1)
+__global__ void __launch_bounds__(Cfg<P, FAST>::THREADS, P == 4 ? (FAST ? 8 : 6) / Cfg<P, FAST>::PPC : 1)
 small3d_kernel(const double* __restrict__ qin, double* __restrict__ qout, const double* __restrict__ cell_size,
                const double* __restrict__ dtv, double* __restrict__ max_eig, unsigned* __restrict__ status,
                int64_t n_patches, Closure cl, const __grid_constant__ CUtensorMap omap) {
-  using C = Cfg<P>;
+  using C = Cfg<P, FAST>;
   constexpr int S = C::S, E = C::E;
   // Odd P: a patch is an odd multiple of 8 bytes, so neither the bulk copies nor the
   // tensor store (16-byte granularity) can address it.  The CTA stages it with 8-byte
@@ -245,9 +246,16 @@ small3d_kernel(const double* __restrict__ qin, double* __restrict__ qout, const 
       Side<3> sd[3];
       bool ok = true;
       if constexpr (FAST) {
+        // (r, p, c) of the volume; the faces reconstruct from it in phase B.  Wave speeds:
+        // max_d |j_d r| + c = (max_d |j_d r|) + c (RN is monotonic)
         const fast::Rpc w = fast::closure<3>(q, cl, ok);
-#pragma unroll
-        for (int d = 0; d < 3; ++d) sd[d].lam = fast::recon<3>(q, w, d, sd[d].f);
+        double* rp = side + (((cz + 1) * E + (cy + 1)) * E + (cx + 1)) * 3;
+        rp[0] = w.r;
+        rp[1] = w.p;
+        rp[2] = w.c;
+        const double u0 = fabs(__dmul_rn(q[1], w.r)), u1 = fabs(__dmul_rn(q[2], w.r)), u2 = fabs(__dmul_rn(q[3], w.r));
+        const double um = speed_max(speed_max(u0, u1), u2);
+        sd[0].lam = sd[1].lam = sd[2].lam = __dadd_rn(um, w.c);
       } else {
         closure_all_ranged<3>(q, cl, sd, ok);
       }
@@ -257,9 +265,11 @@ small3d_kernel(const double* __restrict__ qin, double* __restrict__ qout, const 
       m = v > m ? v : m;
       v = (unsigned long long)__double_as_longlong(sd[2].lam);
       cmax = v > m ? v : m;
-      put_rec<P>(side, 0, cx + 1, cy, cz, sd[0]);
-      put_rec<P>(side, 1, cy + 1, cx, cz, sd[1]);
-      put_rec<P>(side, 2, cz + 1, cx, cy, sd[2]);
+      if constexpr (!FAST) {
+        put_rec<P>(side, 0, cx + 1, cy, cz, sd[0]);
+        put_rec<P>(side, 1, cy + 1, cx, cz, sd[1]);
+        put_rec<P>(side, 2, cz + 1, cx, cy, sd[2]);
+      }
     }
     // ---- A2: face-halo volumes, one direction each, balanced over the CTA's warps ----
     // The PPC x 96 tasks form 3*PPC chunks of 32 (one patch slot, one face pair -> a
@@ -278,10 +288,12 @@ small3d_kernel(const double* __restrict__ qin, double* __restrict__ qout, const 
       bool okh = true;
       if constexpr (FAST) {
         const fast::Rpc w = fast::closure<3>(qh, cl, okh);
-        // constant normals (a run-time n would index qh dynamically: local memory)
-        if (nd == 0) sh.lam = fast::recon<3>(qh, w, 0, sh.f);
-        else if (nd == 1) sh.lam = fast::recon<3>(qh, w, 1, sh.f);
-        else sh.lam = fast::recon<3>(qh, w, 2, sh.f);
+        double* rp = sideb + lpt * C::SIDE + ((hz * E + hy) * E + hx) * 3;
+        rp[0] = w.r;
+        rp[1] = w.p;
+        rp[2] = w.c;
+        if (!okh) atomicOr(&slowflag[g & 1], 1u << lpt);
+        return;
       } else if (nd == 0) {
         closure_one_ranged<3>(qh, cl, 0, sh, okh);
       } else if (nd == 1) {
@@ -341,21 +353,21 @@ small3d_kernel(const double* __restrict__ qin, double* __restrict__ qout, const 
       double qc[S], qn[S], val[S], slo[S], shi[S];
       load(cx + 1, cy + 1, cz + 1, qc);
       const int hcc[3] = {cx + 1, cy + 1, cz + 1};
-      const int ab[3][2] = {{cy, cz}, {cx, cz}, {cx, cy}};
+      auto rpc_at = [&](int hx, int hy, int hz) -> fast::Rpc {
+        const double* rp = side + ((hz * E + hy) * E + hx) * 3;
+        return fast::Rpc{rp[0], rp[1], rp[2]};
+      };
+      const fast::Rpc wc = rpc_at(hcc[0], hcc[1], hcc[2]);
 #pragma unroll
       for (int nd = 0; nd < 3; ++nd) {
         double fc[4], fn[4], G[S];
-        const double lc = side[side_at<P>(nd, 0, hcc[nd], ab[nd][0], ab[nd][1])];
-#pragma unroll
-        for (int k = 0; k < 4; ++k) fc[k] = side[side_at<P>(nd, k + 1, hcc[nd], ab[nd][0], ab[nd][1])];
+        const double lc = fast::recon<3>(qc, wc, nd, fc);
 #pragma unroll
         for (int sh = -1; sh <= 1; sh += 2) {
           int hq[3] = {hcc[0], hcc[1], hcc[2]};
           hq[nd] += sh;
           load(hq[0], hq[1], hq[2], qn);
-          const double ln = side[side_at<P>(nd, 0, hcc[nd] + sh, ab[nd][0], ab[nd][1])];
-#pragma unroll
-          for (int k = 0; k < 4; ++k) fn[k] = side[side_at<P>(nd, k + 1, hcc[nd] + sh, ab[nd][0], ab[nd][1])];
+          const double ln = fast::recon<3>(qn, rpc_at(hq[0], hq[1], hq[2]), nd, fn);
           if (sh < 0) fast::face<3>(G, nd, qn, ln, fn, qc, lc, fc);   // lower face: neighbour below
           else fast::face<3>(G, nd, qc, lc, fc, qn, ln, fn);          // upper face: neighbour above
 #pragma unroll
@@ -459,7 +471,7 @@ small3d_kernel(const double* __restrict__ qin, double* __restrict__ qout, const 
 
 template <int P, bool FAST = false>
 cudaError_t launch(const FvbArgs& a, cudaStream_t st) {
-  using C = Cfg<P>;
+  using C = Cfg<P, FAST>;
   auto kfn = small3d_kernel<P, FAST>;
   cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::BYTES);
   if (e != cudaSuccess) return e;
