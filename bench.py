@@ -515,13 +515,17 @@ def main():
         e2e["pcie_gbs"] = {k: round(v, 2) for k, v in bw.items()}
         e2e["roofline"] = {"bound": "pcie", "value": bound, "frac": e2e["value"] / bound}
 
-    cpu = None
+    cpu = cpu_numpy = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         budget = float(os.environ.get("FVB_BENCH_CPU_SECONDS", "10"))
         rates, cores, m, _ = oracle_steps(host.QIn, host.cell_size, host.dt, dim, p, 3, 1, budget)
         cpu = {"value": statistics.median(rates), "unit": "cell updates/s", "cores": cores, "kind": "port",
                "sample": f"oracle port (C, OpenMP, {cores} threads) on this run's batch: 3 steps of {m} patches "
                          f"({'the full batch' if m == n else 'rotating slices'}), median"}
+        # the reference's own Python CPU path (north star: "next to the reference Python CPU path
+        # timed on the box's own host cores"), on a bounded sample of the same batch
+        if not os.environ.get("FVB_BENCH_NO_NUMPY"):
+            cpu_numpy = numpy_engine_baseline(host.QIn, host.cell_size, host.dt, dim, p)
     del host
 
     if rank == 0:
@@ -555,6 +559,7 @@ def main():
                               "flops_per_cell": flops_cell},
             "exact": exact,
             "cpu_baseline": cpu,
+            "cpu_baseline_numpy": cpu_numpy,
             "e2e": e2e,
             # per timed step: the update kernel (+ the fused path's redo pass) and the dt reduction
             # (one kernel up to 16,384 patches on one GPU, else reduce + set_dt)
