@@ -196,8 +196,9 @@ int fvb_halo_project_window(const fvb_spec* spec, const double* ghost_lo, const 
  * that batch's halo shell from the neighbours' interiors (21 % of the bytes of a full
  * halo projection), and fvb_totals_haloed sums the interiors for the step's totals.
  * Bit-identical to fvb_update + fvb_halo_project.  2D AoS, 2 <= p <= 32. */
+/* flags: bit 0 = zero the status words first; FVB_MODE_FAST = fast mode (2D p = 16, as fvb_update). */
 int fvb_update_to_haloed(const fvb_spec* spec, const double* qin, double* qin_next, const double* cell_size,
-                         const double* dt, double* max_eig, uint32_t* status, int zero_status, void* stream);
+                         const double* dt, double* max_eig, uint32_t* status, int flags, void* stream);
 int fvb_halo_shell(const fvb_spec* spec, double* qin, const int32_t* grid_shape, int periodic, void* stream);
 int fvb_totals_haloed(const fvb_spec* spec, const double* qin, double* scratch, double* totals, void* stream);
 

@@ -295,7 +295,9 @@ int fvb_update_host(const fvb_spec* spec, const double* qin_h, double* qout_h, c
 }
 
 int fvb_update_to_haloed(const fvb_spec* spec, const double* qin, double* qin_next, const double* cell_size,
-                         const double* dt, double* max_eig, uint32_t* status, int zero_status, void* stream) {
+                         const double* dt, double* max_eig, uint32_t* status, int flags, void* stream) {
+  const int zero_status = flags & 1;
+  const bool fast = (flags & FVB_MODE_FAST) != 0;
   int rc = check_spec(spec);
   if (rc) return rc;
   if (spec->n_patches == 0) return FVB_OK;
@@ -320,7 +322,7 @@ int fvb_update_to_haloed(const fvb_spec* spec, const double* qin, double* qin_ne
   a.max_eig = max_eig;
   a.status = status;
   a.out_haloed = 1;
-  e = fvb_launch_fused2d16_warp(a, st);
+  e = fast && fvb_fast2d_supported(2, spec->p, 0) ? fvb_launch_fast2d16(a, st) : fvb_launch_fused2d16_warp(a, st);
   if (e == cudaSuccess) e = fvb_launch_redo(a, st);
   return e == cudaSuccess ? FVB_OK : set_cuda_error(e, "fvb_update_to_haloed");
 }

@@ -201,7 +201,7 @@ class SimulationResult:
 
 def run_simulation(db: DeviceBatch, grid_shape, steps: int, cfl: float = 0.4, periodic: bool = True,
                    kernel="auto", dx: float | None = None, graph: bool | None = None,
-                   direct: bool | None = None, diagnose: bool = True) -> SimulationResult:
+                   direct: bool | None = None, diagnose: bool = True, mode: str = "exact") -> SimulationResult:
     """Device-resident time loop on one GPU.
 
     db.QOut holds the initial interior field of a logical uniform patch grid
@@ -220,6 +220,9 @@ def run_simulation(db: DeviceBatch, grid_shape, steps: int, cfl: float = 0.4, pe
     step counter, so every replay is the same graph.  Results are bit-identical
     to the eager loop (graph=False), which is also the fallback when capture is
     unavailable.
+
+    mode: "exact" (bit-identical to the reference's update, the default) or "fast"
+    (the 1e-12 parity bar; 3D p=16, 2D p=16 and 3D p=4 run the fast kernels).
 
     Errors: a non-physical state raises NonPhysicalStateError with the
     first failing step and -- with diagnose=True (the default, at the cost of one
@@ -249,6 +252,10 @@ def run_simulation(db: DeviceBatch, grid_shape, steps: int, cfl: float = 0.4, pe
     stepper.prepass()
     gmax_h[0].copy_(stepper.gmax[0])
     k_t = torch.zeros(1, dtype=torch.int64, device=dev)    # device step counter (graph mode)
+    from .device import MODES, kernel_id
+
+    kernel_id("auto", mode)                                # validates the mode
+    fast_flag = MODES[mode]                                # fvb_update_to_haloed flags (bit 0 unused here)
     tot_cur = torch.empty(s, **f64)
 
     # 2D AoS fast path: the update writes into the interior of the other haloed buffer,
@@ -268,7 +275,8 @@ def run_simulation(db: DeviceBatch, grid_shape, steps: int, cfl: float = 0.4, pe
         src, dst = bufs[k % 2], bufs[(k + 1) % 2]
         dt_h.index_copy_(0, k_t, stepper.dt_scalar)
         _lib.check(L.fvb_update_to_haloed(fs, _vp(src), _vp(dst), _vp(db.cell_size), _vp(db.dt),
-                                          _vp(db.max_eigenvalue), _vp(db.status), 0, st), "fvb_update_to_haloed")
+                                          _vp(db.max_eigenvalue), _vp(db.status), fast_flag, st),
+                   "fvb_update_to_haloed")
         flag_h.index_copy_(0, k_t, db.status[0:1])
         stepper.reduce_dt()
         _lib.check(L.fvb_halo_shell(fs, _vp(dst), gshape, int(bool(periodic)), st), "fvb_halo_shell")
@@ -279,7 +287,7 @@ def run_simulation(db: DeviceBatch, grid_shape, steps: int, cfl: float = 0.4, pe
 
     def step_body():
         dt_h.index_copy_(0, k_t, stepper.dt_scalar)       # the dt this step advances by
-        db.update(kernel=kernel, zero_status=False)       # status[0] accumulates; the redo list self-empties
+        db.update(kernel=kernel, zero_status=False, mode=mode)   # status[0] accumulates; the redo list self-empties
         flag_h.index_copy_(0, k_t, db.status[0:1])
         stepper.reduce_dt()                               # next step's dt from this step's wave speeds
         db.halo_project_totals(grid_shape, periodic, tot_cur, scratch)   # one pass over QOut
@@ -320,7 +328,7 @@ def run_simulation(db: DeviceBatch, grid_shape, steps: int, cfl: float = 0.4, pe
     gm = gmax_h.cpu().numpy()
     kind, step = _first_failure(flag_h.cpu().numpy()[:steps], gm[:steps])
     if kind == "nonphysical" and init is not None:
-        _raise_located(db, init, grid_shape, step, cfl, periodic, kernel, dx)
+        _raise_located(db, init, grid_shape, step, cfl, periodic, kernel, dx, mode)
     _raise_failure(kind, step, gm)
     res = SimulationResult(db.spec.dimensions)
     res.dt = [float(v) for v in dt_h.cpu().numpy()[:steps]]
@@ -356,7 +364,7 @@ def _raise_failure(kind, step, gm) -> None:
         raise NonPhysicalStateError("non-physical state during run_simulation", step=step)
 
 
-def _raise_located(db, init, grid_shape, step, cfl, periodic, kernel, dx) -> None:
+def _raise_located(db, init, grid_shape, step, cfl, periodic, kernel, dx, mode="exact") -> None:
     """Replay the run (bit-identical, eager) from the saved initial field up to `step`, then
     locate the first inadmissible volume of that step's input (patch-wise order) and raise
     with step, patch and haloed volume."""
@@ -366,7 +374,7 @@ def _raise_located(db, init, grid_shape, step, cfl, periodic, kernel, dx) -> Non
     db.QOut.copy_(init)
     if step > 0:
         run_simulation(db, grid_shape, step, cfl=cfl, periodic=periodic, kernel=kernel, dx=dx, graph=False,
-                       diagnose=False)
+                       diagnose=False, mode=mode)
     else:
         db.halo_project(grid_shape, periodic)
     hit = first_error(db.locate(), Ordering.PATCH_WISE, 1)
@@ -488,21 +496,21 @@ class ShardedGrid:
         exchange_ghost_layers(self.db.QOut, self.layer_elems, self.ghost_lo, self.ghost_hi, self.rank, self.world,
                               self.periodic, self.group)
 
-    def update_and_exchange(self, kernel="auto") -> None:
+    def update_and_exchange(self, kernel="auto", mode: str = "exact") -> None:
         """The step's update with the ghost exchange overlapped: the two boundary layers are
         updated first and sent while the interior layers update (NCCL runs on its own stream,
         ordered after the boundary launches; the ghosts are awaited before the halo)."""
         own_layers = self.l1 - self.l0
         if self.world == 1 or own_layers < 3 or self.db.layout != "aos":
-            self.db.update(kernel=kernel, zero_status=False)
+            self.db.update(kernel=kernel, zero_status=False, mode=mode)
             self.exchange()
             return
         L, n = self.layer, self.db.n_patches
-        self.db.update_range(0, L, kernel)
-        self.db.update_range(n - L, n, kernel)
+        self.db.update_range(0, L, kernel, mode=mode)
+        self.db.update_range(n - L, n, kernel, mode=mode)
         works = exchange_ghost_layers_start(self.db.QOut, self.layer_elems, self.ghost_lo, self.ghost_hi, self.rank,
                                             self.world, self.periodic, self.group)
-        self.db.update_range(L, n - L, kernel)
+        self.db.update_range(L, n - L, kernel, mode=mode)
         for w in works:
             w.wait()
 
@@ -519,7 +527,7 @@ class ShardedGrid:
 
 
 def run_simulation_sharded(sg: ShardedGrid, steps: int, cfl: float = 0.4, kernel="auto",
-                           dx: float | None = None) -> SimulationResult:
+                           dx: float | None = None, mode: str = "exact") -> SimulationResult:
     """run_simulation over a grid sharded across ranks (one GPU each): the same step --
     dt from the global maximum wave speed (one MAX all-reduce), fused update of the own
     patches (the two boundary layers first, so their ghost-layer exchange overlaps the
@@ -560,7 +568,7 @@ def run_simulation_sharded(sg: ShardedGrid, steps: int, cfl: float = 0.4, kernel
     gmax_h[0].copy_(stepper.gmax[0])
     for k in range(steps):
         dt_h[k].copy_(stepper.dt_scalar[0])
-        sg.update_and_exchange(kernel)        # boundary layers first, their exchange overlaps the rest
+        sg.update_and_exchange(kernel, mode)  # boundary layers first, their exchange overlaps the rest
         flag_h[k].copy_(db.status[0])
         stepper.reduce_dt()
         halo_and_totals(k + 1, exchanged=True)

@@ -4,6 +4,7 @@ or with --2d on a 256^2 grid of 2D p=16 patches (65,536 patches, C2's batch).
     python scripts/time_runsim.py          # moving fluid with a random density perturbation
     python scripts/time_runsim.py --sod    # Sod shock tube along x: fluid at rest (exact +0 momentum)
     --eager                                # step by step instead of replaying the captured CUDA graph
+    --fast                                 # mode="fast" (the 1e-12 parity bar)
 """
 import sys
 import time
@@ -31,13 +32,14 @@ else:
     q[...] = state
     q[:, :, 0] += 0.1 * torch.rand(n, p ** dim, device="cuda", dtype=torch.float64)
 db.cell_size.fill_(1.0 / 16)
-driver.run_simulation(db, g, steps=2, graph="--eager" not in sys.argv)
+mode = "fast" if "--fast" in sys.argv else "exact"
+driver.run_simulation(db, g, steps=2, graph="--eager" not in sys.argv, mode=mode)
 torch.cuda.synchronize()
 graph = "--eager" not in sys.argv
 for steps in (10, 40, 200):
     t0 = time.perf_counter()
-    res = driver.run_simulation(db, g, steps=steps, graph=graph)
+    res = driver.run_simulation(db, g, steps=steps, graph=graph, mode=mode)
     torch.cuda.synchronize()
     dt = time.perf_counter() - t0
-    print(f"run_simulation {dim}D {steps} steps: {dt / steps * 1e3:.3f} ms/step, "
+    print(f"run_simulation {dim}D {mode} {steps} steps: {dt / steps * 1e3:.3f} ms/step, "
           f"{n * p**dim * steps / dt / 1e9:.2f} Gcell/s")

@@ -392,3 +392,25 @@ def test_run_simulation_nonphysical_is_located(graph):
     with pytest.raises(NonPhysicalStateError) as ei:
         driver.run_simulation(db, grid, steps=70, cfl=0.4, periodic=True, graph=graph)
     assert (ei.value.step, ei.value.patch, ei.value.volume) == (0, 4, (6, 8)), str(ei.value)
+
+
+@pytest.mark.parametrize("dim,p,grid,direct", [(3, 16, (2, 2, 2), None), (2, 16, (4, 3), True), (2, 16, (4, 3), False),
+                                               (3, 4, (3, 2, 4), None)])
+def test_run_simulation_fast_mode_within_bar(dim, p, grid, direct):
+    """mode="fast" runs the fast kernels inside run_simulation (classic and 2D direct paths):
+    after 12 steps the field, the dt history and the totals are within the north star's
+    1e-12 relative of the exact (bit-identical-to-reference) run."""
+    n = int(np.prod(grid))
+    q = oracle.synthetic_qin(dim, p, n, seed=61).reshape(n, (p + 2) ** dim, dim + 2)
+    inner = q.reshape((n,) + (p + 2,) * dim + (dim + 2,))[(slice(None),) + (slice(1, -1),) * dim].reshape(n, -1)
+    res, fields = [], []
+    for mode in ("exact", "fast"):
+        db = _db_with_field(dim, p, grid, inner)
+        res.append(driver.run_simulation(db, grid, steps=12, cfl=0.4, periodic=True, direct=direct, mode=mode))
+        fields.append(db.QOut.cpu().numpy().reshape(-1, dim + 2))
+    ex, fa = fields
+    rel = np.max(np.abs(fa - ex), axis=0) / np.max(np.abs(ex), axis=0)
+    assert np.all(rel <= 1e-12) and np.all(rel < 1e-13), rel
+    assert np.max(np.abs(np.array(res[1].dt) / np.array(res[0].dt) - 1.0)) < 1e-13
+    t0, t1 = np.asarray(res[0].totals), np.asarray(res[1].totals)
+    assert np.all(np.abs(t1 - t0) <= 1e-12 * np.abs(t0).max(axis=0))
