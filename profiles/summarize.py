@@ -83,13 +83,17 @@ def main():
     for k in KEYS:
         if k in m:
             lines.append(f"| {k} | {m[k][0]} | {m[k][1]} |")
-    rd = float(m["dram__bytes_read.sum"][0].replace(",", "")) if "dram__bytes_read.sum" in m else None
-    wr = float(m["dram__bytes_write.sum"][0].replace(",", "")) if "dram__bytes_write.sum" in m else None
-    unit_r = m.get("dram__bytes_read.sum", ("", ""))[1]
-    if rd is not None and alg:
-        scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(unit_r, 1)
-        lines += ["", f"DRAM traffic per launch: {(rd + wr) * scale / 1e6:.1f} MB vs algorithmic "
-                  f"{alg / 1e6:.1f} MB ({(rd + wr) * scale / alg:.3f}x)"]
+    scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+
+    def nbytes(key):   # each metric carries its own unit (read and write can differ)
+        if key not in m:
+            return None
+        return float(m[key][0].replace(",", "")) * scale.get(m[key][1], 1)
+
+    rd, wr = nbytes("dram__bytes_read.sum"), nbytes("dram__bytes_write.sum")
+    if rd is not None and wr is not None and alg:
+        lines += ["", f"DRAM traffic per launch: {(rd + wr) / 1e6:.1f} MB vs algorithmic "
+                  f"{alg / 1e6:.1f} MB ({(rd + wr) / alg:.3f}x)"]
     lines += ["", "## Warp stall reasons (cycles per issued instruction)", "", "| reason | value |", "|---|---|"]
     for v, k in stalls(m)[:12]:
         lines.append(f"| {k} | {v:.3f} |")
