@@ -343,8 +343,13 @@ def main():
     import torch
     import torch.distributed as dist
 
+    import ctypes
+
+    from paper_2302_09005_b200 import _lib as flib_mod
     from paper_2302_09005_b200 import device as fdev
     from paper_2302_09005_b200 import driver, mesh, pde
+
+    flib = flib_mod.load()
     from paper_2302_09005_b200.kernel import update_patch_batch, variant_from_labels
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -403,6 +408,9 @@ def main():
         if not args.graph:
             m = steps
             ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(m)]
+            for a, b in ev:   # create the events (torch creates them lazily on the first record)
+                a.record(stream)
+                b.record(stream)
         else:
             graph, ev = stepper.make_graph(m, timing=True)
         for _ in range(warmup):
@@ -417,8 +425,12 @@ def main():
             if graph is not None:
                 graph.replay()
                 continue
-            for pair in ev:
-                stepper.step(events=pair)   # the step's update launches bracketed by the pair
+            for a, b in ev:
+                # the step's main kernel bracketed by the pair (recorded inside the C ABI around
+                # the fused kernel, whose last CTA carries the CFL tail; the redo pass launched
+                # after it is excluded): roofline.kernel_ms is "that kernel"
+                flib.fvb_time_next_update(ctypes.c_void_p(a.cuda_event), ctypes.c_void_p(b.cuda_event))
+                stepper.step()
         t1.record(stream)
         torch.cuda.synchronize()
         if world > 1:

@@ -102,6 +102,14 @@ int fvb_update_cfl(const fvb_spec* spec, const double* qin, double* qout, const 
                    double* dt, double* max_eig, uint32_t* status, int kernel, double cfl, double dx,
                    double* gmax, double* dt_scalar, int set_dt, void* stream);
 
+/* Measurement hook (bench.py's per-launch roofline timing): the NEXT fvb_update /
+ * fvb_update_cfl / fvb_update_to_haloed call made by this host thread records the CUDA
+ * event `start` (a cudaEvent_t) on its stream right before its main kernel and `stop`
+ * right after it -- the exact redo pass and the reduce kernels excluded (the CFL tail
+ * that runs in the main kernel's last CTA is included).  One-shot;
+ * either pointer may be NULL. */
+int fvb_time_next_update(void* start, void* stop);
+
 /* Number of uint32 status words fvb_update needs for n patches (2n + 5: flag,
  * redo count, redo list -- sized 2n for kernels that may queue a patch twice --
  * two CTA counters and the CFL-tail mark). */

@@ -35,7 +35,7 @@ EXPORTED = (
     "fvb_host_pin", "fvb_host_unpin", "fvb_update_to_haloed", "fvb_halo_shell", "fvb_totals_haloed",
     "fvb_mgpu_unique_id", "fvb_mgpu_init_rank", "fvb_mgpu_init", "fvb_mgpu_allreduce_max",
     "fvb_mgpu_allreduce_max_all", "fvb_mgpu_finalize", "fvb_totals_scratch_bytes", "fvb_totals",
-    "fvb_fvb1_header", "fvb_fvb1_read", "fvb_fvb1_write",
+    "fvb_fvb1_header", "fvb_fvb1_read", "fvb_fvb1_write", "fvb_time_next_update",
 )
 
 
@@ -98,6 +98,8 @@ def load():
     L.fvb_halo_project_totals.argtypes = [sp, vp, vp, vp, i32, vp, vp, vp]
     L.fvb_halo_project_window.restype = i32
     L.fvb_halo_project_window.argtypes = [sp, vp, vp, vp, vp, vp, i32, i32, vp, vp, vp]
+    L.fvb_time_next_update.restype = i32
+    L.fvb_time_next_update.argtypes = [vp, vp]
     L.fvb_update_to_haloed.restype = i32
     L.fvb_update_to_haloed.argtypes = [sp, vp, vp, vp, vp, vp, vp, i32, vp]
     L.fvb_halo_shell.restype = i32

@@ -72,6 +72,22 @@ int fvb_select_kernel(const fvb_spec* spec) {
 
 }  // extern "C"
 
+// ---- measurement hook: fvb_time_next_update ----
+static thread_local cudaEvent_t t_ev_start = nullptr, t_ev_stop = nullptr;
+void fvb_timing_mark_start(cudaStream_t st) {
+  if (t_ev_start) cudaEventRecord(t_ev_start, st);
+  t_ev_start = nullptr;
+}
+void fvb_timing_mark_stop(cudaStream_t st) {
+  if (t_ev_stop) cudaEventRecord(t_ev_stop, st);
+  t_ev_stop = nullptr;
+}
+extern "C" int fvb_time_next_update(void* start, void* stop) {
+  t_ev_start = static_cast<cudaEvent_t>(start);
+  t_ev_stop = static_cast<cudaEvent_t>(stop);
+  return FVB_OK;
+}
+
 namespace {
 // fvb_update / fvb_update_cfl.  With tail != nullptr (fvb_update_cfl) the step also reduces
 // max_eig to *tail->gmax and optionally sets dt: inside the redo pass when the fused path
@@ -115,6 +131,7 @@ int update_impl(const fvb_spec* spec, const double* qin, double* qout, const dou
     a.dt_patches = tail->tail_dt ? dt : nullptr;
     a.tail_dt = tail->tail_dt;
   }
+  fvb_timing_mark_start(st);   // (measurement hook: the main kernel starts here)
   if (k == FVB_KERNEL_GENERIC) {
     // per-patch maxima are combined with atomicMax on the bit patterns
     e = cudaMemsetAsync(max_eig, 0, sizeof(double) * (size_t)spec->n_patches, st);
@@ -131,6 +148,7 @@ int update_impl(const fvb_spec* spec, const double* qin, double* qout, const dou
   } else {
     e = fvb_launch_fused16(a, st);
   }
+  fvb_timing_mark_stop(st);   // no redo pass (generic kernel): the stop mark is still pending
   if (e == cudaSuccess && tail && !tail_in_redo)
     e = fvb_launch_reduce_dt(max_eig, spec->n_patches, tail->cfl, tail->dx, tail->gmax, tail->dt_scalar,
                              tail->tail_dt ? dt : nullptr, tail->tail_dt, st);
@@ -322,6 +340,7 @@ int fvb_update_to_haloed(const fvb_spec* spec, const double* qin, double* qin_ne
   a.max_eig = max_eig;
   a.status = status;
   a.out_haloed = 1;
+  fvb_timing_mark_start(st);
   e = fast && fvb_fast2d_supported(2, spec->p, 0) ? fvb_launch_fast2d16(a, st) : fvb_launch_fused2d16_warp(a, st);
   if (e == cudaSuccess) e = fvb_launch_redo(a, st);
   return e == cudaSuccess ? FVB_OK : set_cuda_error(e, "fvb_update_to_haloed");

@@ -41,6 +41,10 @@ bool fvb_fused2d_warp_supported(int p);
 bool fvb_fast3d_supported(int dim, int p, int layout);
 cudaError_t fvb_launch_fast3d16(const FvbArgs& a, cudaStream_t st);
 bool fvb_fast2d_supported(int dim, int p, int layout);
+// measurement hook (fvb_time_next_update): record the pending start / stop event of this
+// thread's next update around its main kernel (the redo pass calls the stop mark first)
+void fvb_timing_mark_start(cudaStream_t st);
+void fvb_timing_mark_stop(cudaStream_t st);
 bool fvb_fast_small3d_supported(int dim, int p, int layout);
 cudaError_t fvb_launch_fast_small3d(const FvbArgs& a, cudaStream_t st);   // includes its redo pass
 cudaError_t fvb_launch_fast2d16(const FvbArgs& a, cudaStream_t st);
