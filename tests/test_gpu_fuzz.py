@@ -151,3 +151,71 @@ def test_fuzz_halo_project_vs_oracle(seed):
                                           device._stream_handle(torch, None)), "unpack")
         got = out.cpu().numpy()
     assert_bits_equal(got.reshape(ref.shape), ref, f"seed {seed}: {dim}D p={p} grid={grid} {layout} periodic={periodic}")
+
+
+FAST_SHAPES = [(3, 16), (2, 16), (3, 4)]
+
+
+def _fast_case(seed):
+    """The sweep's value sets on the shapes with a fast kernel (AoS, kernel auto)."""
+    rng = np.random.default_rng(10_000 + seed)
+    dim, p = FAST_SHAPES[seed % len(FAST_SHAPES)]
+    gamma = float(rng.choice([1.4, 5.0 / 3.0]))
+    v = (p + 2) ** dim
+    n = int(rng.integers(1, max(2, min(300, 40000 // p ** dim))))
+    scale = 10.0 ** rng.uniform(-30, 30) if rng.random() < 0.2 else 1.0
+    rho = rng.uniform(0.5, 2.0, (n, v)) * scale
+    vel = rng.uniform(-1.0, 1.0, (n, v, dim))
+    pr = rng.uniform(0.5, 2.0, (n, v)) * scale
+    m = rng.random()
+    if m < 0.3:
+        vel[rng.random((n, v, dim)) < 0.4] = 0.0
+    elif m < 0.4:
+        vel[rng.random((n, v, dim)) < 0.3] = -0.0
+    elif m < 0.5:
+        vel[rng.random((n, v, dim)) < 0.05] = 1e-70
+    q = np.empty((n, v, dim + 2))
+    q[..., 0] = rho
+    q[..., 1:1 + dim] = rho[..., None] * vel
+    q[..., -1] = pr / (gamma - 1.0) + 0.5 * rho * np.sum(vel * vel, axis=-1)
+    if rng.random() < 0.1:
+        q[rng.integers(n), rng.integers(v), -1] = -1.0 * scale
+    cs = rng.uniform(0.25, 4.0, n)
+    dt = rng.uniform(0.0, 0.4, n) * (cs / p) / (np.sqrt(gamma * 4.0) + 1.0)
+    dt[rng.random(n) < 0.1] = 0.0
+    return dim, p, n, gamma, q.reshape(n, -1), cs, dt
+
+
+@pytest.mark.parametrize("seed", range(48))
+def test_fuzz_fast_mode_vs_oracle(seed):
+    """mode="fast" over random value sets: the non-physical flag as the reference, and -- when the
+    reference succeeds -- QOut per patch and max_eigenvalue within 1e-12 relative (NaN / inf
+    positions identical)."""
+    dim, p, n, gamma, qin, cs, dt = _fast_case(seed)
+    spec = mesh.PatchSpec(dim, p, dim + 2)
+    b = mesh.make_patch_batch(spec, n)
+    b.QIn[...] = qin
+    b.cell_size[...] = cs[:, None]
+    b.dt[...] = dt
+    ref_q, ref_l, st = oracle.update(dim, p, gamma, b.QIn, b.cell_size, b.dt)
+    db = device.DeviceBatch.from_host(b, gamma)
+    db.update(mode="fast")
+    out = mesh.make_patch_batch(spec, n)
+    db.to_host(out)
+    what = f"seed {seed}: {dim}D p={p} n={n} gamma={gamma:.3f}"
+    assert db.nonphysical() == (st != 0), what
+    if st != 0:
+        return
+    s = dim + 2
+    fin = np.isfinite(ref_q)
+    assert np.array_equal(np.isfinite(out.QOut), fin), what
+    a, r = np.where(fin, out.QOut, 0.0), np.where(fin, ref_q, 0.0)
+    for k in range(n):   # per patch: scales differ by up to 1e60 across a batch
+        ak, rk = a[k].reshape(-1, s), r[k].reshape(-1, s)
+        num = np.max(np.abs(ak - rk), axis=0)
+        den = np.maximum(np.max(np.abs(rk), axis=0), np.finfo(np.float64).tiny)
+        assert np.max(num / den) <= 1e-12, (what, k, np.max(num / den))
+    lf = np.isfinite(ref_l)
+    assert np.array_equal(np.isfinite(out.max_eigenvalue), lf), what
+    rel = np.abs(out.max_eigenvalue[lf] - ref_l[lf]) / np.maximum(np.abs(ref_l[lf]), np.finfo(np.float64).tiny)
+    assert rel.size == 0 or rel.max() <= 1e-12, (what, rel.max())
