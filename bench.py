@@ -11,17 +11,18 @@ configuration's full patch count; --scaling strong splits it over the ranks.
 
 Rank 0 prints one JSON line (the driver contract):
   value        device-timed throughput of the K steps (CUDA events, max over ranks)
-               in --mode (default "fast": QOut within the north star's 1e-12
-               relative tolerance, max_eigenvalue bit-exact; tests/test_gpu_fast.py)
+               in --mode (default "fast": QOut and max_eigenvalue within the north
+               star's 1e-12 relative tolerance; tests/test_gpu_fast.py)
   exact        the same for the bit-exact mode (the library's default)
   e2e          the drop-in public API (kernel.update_patch_batch) on pinned host
                arrays, H2D + D2H inside the timed region
   roofline     the update kernel's algorithmic HBM bytes per launch over its
-               duration, timed by CUDA events around every update inside the
-               replayed graph (the last graph of the timed region), against
-               MEASURED_PEAKS.json
+               duration: the median of CUDA-event pairs recorded on its stream around
+               the main kernel of every timed step (inside the C ABI,
+               fvb_time_next_update), against MEASURED_PEAKS.json
   cpu_baseline the CPU oracle (a C restatement of the reference algorithm, oracle/)
-               over the full configuration batch, on this box's host cores
+               over the full configuration batch, on this box's host cores;
+               cpu_baseline_numpy the reference's own numpy engine (baseline/_ref)
 """
 
 from __future__ import annotations
@@ -48,7 +49,7 @@ CONFIGS = {
     "x3p8": (3, 8, 32768, None),
 }
 METRIC = "cell updates/sec (fp64, 3D Euler p=16) at 1/2/4/8 B200; % of HBM roofline"
-MODE_NOTE = {"fast": "fast (QOut within 1e-12 relative max-norm of the reference, max_eigenvalue bit-exact)",
+MODE_NOTE = {"fast": "fast (QOut and max_eigenvalue within 1e-12 relative of the reference; measured ~1e-16)",
              "exact": "exact (bit-identical to the reference)"}
 
 
