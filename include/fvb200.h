@@ -40,7 +40,7 @@ extern "C" {
 #define FVB_KERNEL_AUTO 0     /* the shape's fused kernel when it has one, else generic */
 #define FVB_KERNEL_GENERIC 1  /* any d, p */
 #define FVB_KERNEL_FUSED 2    /* 2D/3D p == 16 (AoS or SoA), 3D p == 2, 4..8 (AoS), 2D p == 2..32 (AoS) */
-/* OR'ed into the kernel selector: "fast" mode (3D and 2D p = 16, AoS).  QOut and
+/* OR'ed into the kernel selector: "fast" mode (AoS: 3D p = 16, 3D p = 2, 4..8, 2D p = 2..32).  QOut and
  * max_eig within 1e-12 relative per unknown of the reference (the north star's
  * parity bar; measured ~1e-16 / a few ulp).  Shapes without a fast kernel run the
  * exact one (trivially within the bar).  Without the flag every result is

@@ -541,10 +541,23 @@ cudaError_t fvb_launch_fused2d16_warp(const FvbArgs& a, cudaStream_t st) {
   }
 }
 
-// mode "fast" (fvb_fast.cuh): 2D p = 16 AoS (BASELINE configs[1]); other shapes run the exact kernels
-bool fvb_fast2d_supported(int dim, int p, int layout) { return dim == 2 && p == 16 && layout == fvb::kAoS; }
+// mode "fast" (fvb_fast.cuh): every 2D AoS shape the warp kernel takes (p = 2 .. 32)
+bool fvb_fast2d_supported(int dim, int p, int layout) {
+  return dim == 2 && layout == fvb::kAoS && fvb_fused2d_warp_supported(p);
+}
 
 cudaError_t fvb_launch_fast2d16(const FvbArgs& a, cudaStream_t st) {
+  using namespace fvb::f2w;
   if (a.n <= 0) return cudaSuccess;
-  return fvb::f2w::launch<16, true>(a, st);
+  switch (a.p) {
+#define FVB_P(k) \
+  case k:        \
+    return launch<k, true>(a, st);
+    FVB_P(2) FVB_P(3) FVB_P(4) FVB_P(5) FVB_P(6) FVB_P(7) FVB_P(8) FVB_P(9) FVB_P(10) FVB_P(11) FVB_P(12)
+    FVB_P(13) FVB_P(14) FVB_P(15) FVB_P(16) FVB_P(17) FVB_P(18) FVB_P(19) FVB_P(20) FVB_P(21) FVB_P(22)
+    FVB_P(23) FVB_P(24) FVB_P(25) FVB_P(26) FVB_P(27) FVB_P(28) FVB_P(29) FVB_P(30) FVB_P(31) FVB_P(32)
+#undef FVB_P
+    default:
+      return cudaErrorInvalidValue;
+  }
 }

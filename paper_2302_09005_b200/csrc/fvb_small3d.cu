@@ -533,12 +533,21 @@ cudaError_t fvb_launch_small3d(const FvbArgs& a, cudaStream_t st) {
   return fvb_launch_redo(a, st);
 }
 
-// mode "fast" (fvb_fast.cuh): 3D p = 4 AoS (BASELINE configs[3]); other small shapes run exact
-bool fvb_fast_small3d_supported(int dim, int p, int layout) { return dim == 3 && p == 4 && layout == fvb::kAoS; }
+// mode "fast" (fvb_fast.cuh): every shape the small-patch kernel takes (3D AoS p = 2, 4 .. 8)
+bool fvb_fast_small3d_supported(int dim, int p, int layout) { return fvb_small3d_supported(dim, p, layout); }
 
 cudaError_t fvb_launch_fast_small3d(const FvbArgs& a, cudaStream_t st) {
   if (a.n <= 0) return cudaSuccess;
-  const cudaError_t e = fvb::fs::launch<4, true>(a, st);
+  cudaError_t e;
+  switch (a.p) {
+    case 2: e = fvb::fs::launch<2, true>(a, st); break;
+    case 4: e = fvb::fs::launch<4, true>(a, st); break;
+    case 5: e = fvb::fs::launch<5, true>(a, st); break;
+    case 6: e = fvb::fs::launch<6, true>(a, st); break;
+    case 7: e = fvb::fs::launch<7, true>(a, st); break;
+    case 8: e = fvb::fs::launch<8, true>(a, st); break;
+    default: return cudaErrorInvalidValue;
+  }
   if (e != cudaSuccess) return e;
   return fvb_launch_redo(a, st);
 }

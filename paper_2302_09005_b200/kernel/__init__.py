@@ -215,7 +215,8 @@ def update_patch_batch(batch: PatchBatch, pde: PdeDefinition, variant: KernelVar
     "fast" (QOut and max_eigenvalue within 1e-12 relative per unknown -- the
     north star's parity bar; measured ~1e-16 -- with face-shared fluxes and one
     closure per volume: csrc/fvb_fast3d.cu for 3D p = 16, the FAST warp kernel
-    of csrc/fvb_fused2d_warp.cu for 2D p = 16).  Shapes without a fast kernel
+    of csrc/fvb_fused2d_warp.cu for 2D p = 2..32, the FAST small-patch kernel of
+    csrc/fvb_small3d.cu for 3D p = 2, 4..8; AoS).  Shapes without a fast kernel
     run the exact one.
     """
     if batch.n_patches == 0:

@@ -207,8 +207,9 @@ def test_fast_error_semantics(case):
 
 
 def test_fast_mode_other_shapes_fall_back_to_exact():
-    """No fast kernel for p != 16: mode="fast" runs the exact kernels (bitwise)."""
-    for dim, p, n in [(2, 17, 40), (2, 8, 30), (3, 6, 20), (3, 7, 5)]:
+    """Shapes without a fast kernel (the generic kernel's: 3D p=3, p > 8 but 16, 2D p > 32)
+    run the exact kernels in mode="fast" (bitwise)."""
+    for dim, p, n in [(2, 40, 6), (3, 3, 30), (3, 9, 4), (3, 12, 2)]:
         b = mesh.make_patch_batch(mesh.PatchSpec(dim, p, dim + 2), n)
         b.QIn[...] = oracle.synthetic_qin(dim, p, n, seed=3)
         b.dt[...] = 0.4 * (1.0 / p) / 3.4
@@ -216,6 +217,31 @@ def test_fast_mode_other_shapes_fall_back_to_exact():
         update_patch_batch(b, pde.make_euler_pde(dim), PW, mode="fast")
         assert_bits_equal(b.QOut, ref_q, f"{dim}D p={p}")
         assert_bits_equal(b.max_eigenvalue, ref_l, "max_eig")
+
+
+FAST_ALL = [(2, p) for p in range(2, 33)] + [(3, p) for p in (2, 4, 5, 6, 7, 8)]
+
+
+@pytest.mark.parametrize("dim,p", FAST_ALL, ids=lambda v: str(v))
+def test_fast_every_shape_vs_oracle(dim, p):
+    """mode="fast" on every shape with a fast kernel (2D p = 2..32: the FAST warp kernel;
+    3D p = 2, 4..8: the FAST small-patch kernel): random batches within 1e-12 of the
+    oracle, a constant state bitwise."""
+    n = max(1, min(257, 30000 // p ** dim))
+    b = _batch(n, 100 + 7 * p + dim, p=p, dim=dim)
+    ref_q, ref_l, st = oracle.update(dim, p, 1.4, b.QIn, b.cell_size, b.dt)
+    assert st == 0
+    db, out = _fast_device(b)
+    assert not db.nonphysical()
+    err = rel_maxnorm(out.QOut, ref_q, dim + 2)
+    assert err <= TOL and err < 1e-14, err
+    assert_max_eig_close(out.max_eigenvalue, ref_l)
+    c = mesh.make_patch_batch(mesh.PatchSpec(dim, p, dim + 2), 5)
+    c.qin_view()[...] = pde.euler_state(1.3, [0.2, -0.4, 0.1][:dim], 0.9)
+    c.dt[...] = 0.01
+    _, outc = _fast_device(c)
+    inner = (slice(None),) + (slice(1, -1),) * dim
+    assert_bits_equal(outc.QOut, c.qin_view()[inner].reshape(5, -1), "constant state")
 
 
 def test_unknown_mode_is_a_contract_violation():
