@@ -57,7 +57,7 @@ struct Cfg {
   static constexpr int OFF_OUT = (OFF_SIDE + PPC * SIDE + 15) / 16 * 16;
   // output staging: NOB buffers (1: the store of iteration g-1 must have read it
   // before phase B of iteration g writes; checked before the mid-iteration barrier)
-  static constexpr int NOB = FVB_SMALL3D_NOB;
+  static constexpr int NOB = FAST ? 1 : FVB_SMALL3D_NOB;   // FAST: one buffer measured 1.5 % faster (C4)
   static constexpr int OFF_WMAX = OFF_OUT + NOB * OUTN;
   static constexpr int OFF_FLAG = OFF_WMAX + 2 * (THREADS / 32);   // wmax double-buffered
   static constexpr int OFF_BAR = OFF_FLAG + 1;   // two 32-bit flag words
