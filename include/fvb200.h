@@ -102,6 +102,14 @@ int fvb_update_cfl(const fvb_spec* spec, const double* qin, double* qout, const 
                    double* dt, double* max_eig, uint32_t* status, int kernel, double cfl, double dx,
                    double* gmax, double* dt_scalar, int set_dt, void* stream);
 
+/* run_simulation's per-step history record, one single-thread launch on `stream`: with
+ * k = *step (a device int64), flag_hist[k] = status[0] (the sticky non-physical flag),
+ * dt_hist[k+1] = *dt_scalar (the next step's dt), gmax_hist[k+1] = *gmax,
+ * totals_hist[(k+1)*unknowns + u] = totals[u], then *step = k + 1.  All device pointers. */
+int fvb_step_record(int64_t* step, const double* dt_scalar, const uint32_t* status, const double* totals,
+                    int unknowns, const double* gmax, double* dt_hist, int32_t* flag_hist, double* totals_hist,
+                    double* gmax_hist, void* stream);
+
 /* Measurement hook (bench.py's per-launch roofline timing): the NEXT fvb_update /
  * fvb_update_cfl / fvb_update_to_haloed call made by this host thread records the CUDA
  * event `start` (a cudaEvent_t) on its stream right before its main kernel and `stop`

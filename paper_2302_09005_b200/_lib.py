@@ -36,6 +36,7 @@ EXPORTED = (
     "fvb_mgpu_unique_id", "fvb_mgpu_init_rank", "fvb_mgpu_init", "fvb_mgpu_allreduce_max",
     "fvb_mgpu_allreduce_max_all", "fvb_mgpu_finalize", "fvb_totals_scratch_bytes", "fvb_totals",
     "fvb_fvb1_header", "fvb_fvb1_read", "fvb_fvb1_write", "fvb_time_next_update",
+    "fvb_step_record",
 )
 
 
@@ -98,6 +99,8 @@ def load():
     L.fvb_halo_project_totals.argtypes = [sp, vp, vp, vp, i32, vp, vp, vp]
     L.fvb_halo_project_window.restype = i32
     L.fvb_halo_project_window.argtypes = [sp, vp, vp, vp, vp, vp, i32, i32, vp, vp, vp]
+    L.fvb_step_record.restype = i32
+    L.fvb_step_record.argtypes = [vp, vp, vp, vp, i32, vp, vp, vp, vp, vp, vp]
     L.fvb_time_next_update.restype = i32
     L.fvb_time_next_update.argtypes = [vp, vp]
     L.fvb_update_to_haloed.restype = i32

@@ -82,6 +82,16 @@ void fvb_timing_mark_stop(cudaStream_t st) {
   if (t_ev_stop) cudaEventRecord(t_ev_stop, st);
   t_ev_stop = nullptr;
 }
+extern "C" int fvb_step_record(int64_t* step, const double* dt_scalar, const uint32_t* status, const double* totals,
+                               int unknowns, const double* gmax, double* dt_hist, int32_t* flag_hist,
+                               double* totals_hist, double* gmax_hist, void* stream) {
+  if (!step || !dt_scalar || !status || !totals || !gmax || !dt_hist || !flag_hist || !totals_hist || !gmax_hist ||
+      unknowns < 1)
+    return set_contract("step_record: null buffer or unknowns < 1");
+  const cudaError_t e = fvb_launch_step_record(step, dt_scalar, status, totals, unknowns, gmax, dt_hist, flag_hist,
+                                               totals_hist, gmax_hist, as_stream(stream));
+  return e == cudaSuccess ? FVB_OK : set_cuda_error(e, "fvb_step_record");
+}
 extern "C" int fvb_time_next_update(void* start, void* stop) {
   t_ev_start = static_cast<cudaEvent_t>(start);
   t_ev_stop = static_cast<cudaEvent_t>(stop);

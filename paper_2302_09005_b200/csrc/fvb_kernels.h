@@ -34,6 +34,9 @@ struct FvbArgs {
 constexpr int64_t kTailMaxPatches = 16384;   // one CTA reduces max_eig within the redo pass
 
 cudaError_t fvb_launch_generic(const FvbArgs& a, cudaStream_t st);
+cudaError_t fvb_launch_step_record(int64_t* step, const double* dt_scalar, const unsigned* status,
+                                   const double* totals, int s, const double* gmax, double* dt_hist, int* flag_hist,
+                                   double* totals_hist, double* gmax_hist, cudaStream_t st);
 cudaError_t fvb_launch_fused16(const FvbArgs& a, cudaStream_t st);
 cudaError_t fvb_launch_fused3d16_half(const FvbArgs& a, cudaStream_t st);
 cudaError_t fvb_launch_fused2d16_warp(const FvbArgs& a, cudaStream_t st);

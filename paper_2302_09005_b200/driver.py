@@ -222,16 +222,18 @@ def run_simulation(db: DeviceBatch, grid_shape, steps: int, cfl: float = 0.4, pe
     unavailable.
 
     mode: "exact" (bit-identical to the reference's update, the default) or "fast"
-    (the 1e-12 parity bar; 3D p=16, 2D p=16 and 3D p=4 run the fast kernels).
+    (the 1e-12 parity bar; the shapes with a fast kernel run it).
 
     Errors: a non-physical state raises NonPhysicalStateError with the
     first failing step and -- with diagnose=True (the default, at the cost of one
     device copy of the initial field) -- its patch and haloed volume, found by
     replaying the run bit-identically up to that step and running the locator on its
     input; a step whose global maximum wave speed is <= 0 (dt = cfl*dx/0) raises
-    TimeStepUnderflowError.  The step is GPU-bound (the host enqueues ahead), so the graph
-    saves ~1 % per step against a ~3 ms capture: the default (None) replays a
-    graph for runs of 64 steps or more.
+    TimeStepUnderflowError.
+
+    Per step the device sees the update (fused kernel + redo pass), the dt reduction,
+    the fused halo projection / totals and one fvb_step_record launch that writes the
+    step's history entries and advances the device step counter (no PyTorch kernels).
     """
     import numpy as np
 
@@ -241,8 +243,8 @@ def run_simulation(db: DeviceBatch, grid_shape, steps: int, cfl: float = 0.4, pe
     f64 = dict(dtype=torch.float64, device=dev)
     tot_h = torch.empty((steps + 1, s), **f64)
     gmax_h = torch.empty(steps + 1, **f64)
-    dt_h = torch.empty(max(steps, 1), **f64)
-    flag_h = torch.zeros(max(steps, 1), dtype=torch.int32, device=dev)
+    dt_h = torch.empty(steps + 1, **f64)      # dt_h[k] = the dt step k advances by
+    flag_h = torch.zeros(steps + 1, dtype=torch.int32, device=dev)
     scratch = db.totals_scratch()
 
     init = db.QOut.clone() if diagnose and steps > 0 else None   # replayed on the error path only
@@ -251,6 +253,7 @@ def run_simulation(db: DeviceBatch, grid_shape, steps: int, cfl: float = 0.4, pe
     stepper = CflStepper(db, cfl=cfl, dx=dx, kernel=kernel)
     stepper.prepass()
     gmax_h[0].copy_(stepper.gmax[0])
+    dt_h[0].copy_(stepper.dt_scalar[0])
     k_t = torch.zeros(1, dtype=torch.int64, device=dev)    # device step counter (graph mode)
     from .device import MODES, kernel_id
 
@@ -266,34 +269,30 @@ def run_simulation(db: DeviceBatch, grid_shape, steps: int, cfl: float = 0.4, pe
     bufs = [db.QIn, torch.empty_like(db.QIn)] if direct else None
     gshape = (ctypes.c_int32 * 3)(*(list(grid_shape) + [1] * (3 - len(grid_shape))))
 
-    def direct_step(k):
-        from .device import _stream_handle as _sh
+    def record():
+        """flag_h[k] = status[0]; dt_h[k+1], gmax_h[k+1], tot_h[k+1]; k += 1 (one launch)."""
+        _lib.check(_lib.load().fvb_step_record(
+            _vp(k_t), _vp(stepper.dt_scalar), _vp(db.status), _vp(tot_cur), s, _vp(stepper.gmax), _vp(dt_h),
+            _vp(flag_h), _vp(tot_h), _vp(gmax_h), _stream_handle(torch, None)), "fvb_step_record")
 
+    def direct_step(k):
         L = _lib.load()
         fs = ctypes.byref(db.fvb_spec())
-        st = _sh(torch, None)
+        st = _stream_handle(torch, None)
         src, dst = bufs[k % 2], bufs[(k + 1) % 2]
-        dt_h.index_copy_(0, k_t, stepper.dt_scalar)
         _lib.check(L.fvb_update_to_haloed(fs, _vp(src), _vp(dst), _vp(db.cell_size), _vp(db.dt),
                                           _vp(db.max_eigenvalue), _vp(db.status), fast_flag, st),
                    "fvb_update_to_haloed")
-        flag_h.index_copy_(0, k_t, db.status[0:1])
         stepper.reduce_dt()
         _lib.check(L.fvb_halo_shell(fs, _vp(dst), gshape, int(bool(periodic)), st), "fvb_halo_shell")
         _lib.check(L.fvb_totals_haloed(fs, _vp(dst), _vp(scratch), _vp(tot_cur), st), "fvb_totals_haloed")
-        k_t.add_(1)
-        tot_h.index_copy_(0, k_t, tot_cur[None])
-        gmax_h.index_copy_(0, k_t, stepper.gmax)
+        record()
 
     def step_body():
-        dt_h.index_copy_(0, k_t, stepper.dt_scalar)       # the dt this step advances by
         db.update(kernel=kernel, zero_status=False, mode=mode)   # status[0] accumulates; the redo list self-empties
-        flag_h.index_copy_(0, k_t, db.status[0:1])
         stepper.reduce_dt()                               # next step's dt from this step's wave speeds
         db.halo_project_totals(grid_shape, periodic, tot_cur, scratch)   # one pass over QOut
-        k_t.add_(1)
-        tot_h.index_copy_(0, k_t, tot_cur[None])
-        gmax_h.index_copy_(0, k_t, stepper.gmax)
+        record()
 
     g = None
     if graph is None:
