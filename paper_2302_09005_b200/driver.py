@@ -542,36 +542,40 @@ def run_simulation_sharded(sg: ShardedGrid, steps: int, cfl: float = 0.4, kernel
     f64 = dict(dtype=torch.float64, device=db.device)
     tot_h = torch.empty((steps + 1, s), **f64)
     gmax_h = torch.empty(steps + 1, **f64)
-    dt_h = torch.empty(max(steps, 1), **f64)
-    flag_h = torch.zeros(max(steps, 1), dtype=torch.int32, device=db.device)
+    dt_h = torch.empty(steps + 1, **f64)
+    flag_h = torch.zeros(steps + 1, dtype=torch.int32, device=db.device)
+    tot_cur = torch.empty(s, **f64)
+    k_t = torch.zeros(1, dtype=torch.int64, device=db.device)
     scratch = db.totals_scratch()
     multi = sg.world > 1
 
-    def halo_and_totals(k, exchanged=False):
+    def halo_and_totals(out, exchanged=False):
         if exchanged:
-            sg.halo_only(tot_h[k], scratch)
+            sg.halo_only(out, scratch)
         else:
-            sg.halo(tot_h[k], scratch)
+            sg.halo(out, scratch)
         if multi:   # global totals: gather the shards' vectors, sum in rank order (deterministic)
             parts = [torch.empty(s, **f64) for _ in range(sg.world)]
-            dist.all_gather(parts, tot_h[k].contiguous(), group=sg.group)
+            dist.all_gather(parts, out.contiguous(), group=sg.group)
             acc = parts[0].clone()
             for t in parts[1:]:
                 acc += t
-            tot_h[k].copy_(acc)
+            out.copy_(acc)
 
-    halo_and_totals(0)
+    halo_and_totals(tot_h[0])
     db.status.zero_()
     stepper = CflStepper(db, cfl=cfl, dx=dx, kernel=kernel, group=sg.group)
     stepper.prepass()
     gmax_h[0].copy_(stepper.gmax[0])
-    for k in range(steps):
-        dt_h[k].copy_(stepper.dt_scalar[0])
+    dt_h[0].copy_(stepper.dt_scalar[0])
+    L = _lib.load()
+    for _ in range(steps):
         sg.update_and_exchange(kernel, mode)  # boundary layers first, their exchange overlaps the rest
-        flag_h[k].copy_(db.status[0])
         stepper.reduce_dt()
-        halo_and_totals(k + 1, exchanged=True)
-        gmax_h[k + 1].copy_(stepper.gmax[0])
+        halo_and_totals(tot_cur, exchanged=True)
+        _lib.check(L.fvb_step_record(_vp(k_t), _vp(stepper.dt_scalar), _vp(db.status), _vp(tot_cur), s,
+                                     _vp(stepper.gmax), _vp(dt_h), _vp(flag_h), _vp(tot_h), _vp(gmax_h),
+                                     _stream_handle(torch, None)), "fvb_step_record")
 
     flags = flag_h.clone()
     if multi:
