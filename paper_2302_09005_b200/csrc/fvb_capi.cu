@@ -82,6 +82,11 @@ void fvb_timing_mark_stop(cudaStream_t st) {
   if (t_ev_stop) cudaEventRecord(t_ev_stop, st);
   t_ev_stop = nullptr;
 }
+// the hook is one-shot per update call: whatever the call did (or an early contract
+// error), nothing stays armed for a later call
+struct TimingHookScope {
+  ~TimingHookScope() { t_ev_start = t_ev_stop = nullptr; }
+};
 extern "C" int fvb_step_record(int64_t* step, const double* dt_scalar, const uint32_t* status, const double* totals,
                                int unknowns, const double* gmax, double* dt_hist, int32_t* flag_hist,
                                double* totals_hist, double* gmax_hist, void* stream) {
@@ -104,6 +109,7 @@ namespace {
 // runs one and the batch is small enough for one CTA, else with the reduce kernels.
 int update_impl(const fvb_spec* spec, const double* qin, double* qout, const double* cell_size, double* dt,
                 double* max_eig, uint32_t* status, int kernel, int zero_status, const FvbArgs* tail, void* stream) {
+  const TimingHookScope hook_scope;
   int rc = check_spec(spec);
   if (rc) return rc;
   if (spec->n_patches == 0) return FVB_OK;   // kernel/__init__.py:123-124
@@ -324,6 +330,7 @@ int fvb_update_host(const fvb_spec* spec, const double* qin_h, double* qout_h, c
 
 int fvb_update_to_haloed(const fvb_spec* spec, const double* qin, double* qin_next, const double* cell_size,
                          const double* dt, double* max_eig, uint32_t* status, int flags, void* stream) {
+  const TimingHookScope hook_scope;
   const int zero_status = flags & 1;
   const bool fast = (flags & FVB_MODE_FAST) != 0;
   int rc = check_spec(spec);
