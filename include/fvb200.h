@@ -78,13 +78,13 @@ int fvb_select_kernel(const fvb_spec* spec);
  *   cell_size  [N*dim]  only cell_size[patch*dim + 0] is read (vectorized.py:169)
  *   dt         [N]      per-patch time step, must be >= 0 (checked by the host)
  *   max_eig    [N]      per-patch max directional wave speed (written, vectorized.py:226-231)
- *   status     [2N+5]   device words (fvb_status_words), zero-initialised once by the caller:
+ *   status     [2N+8]   device words (fvb_status_words), zero-initialised once by the caller:
  *                       status[0] is ORed with 1 when a face-box volume has rho <= 0 or
  *                       p < 0 (sticky: clear it with zero_status = 1 or a memset);
  *                       status[1] / status[2..2N+1] are the redo list the fused kernels use
  *                       for patches whose quotients need CUDA's division slow path
- *                       (re-evaluated exactly before returning); status[2N+2 .. 2N+4] are
- *                       CTA counters and a mark of the CFL tail (csrc/fvb_tail.cuh).  The
+ *                       (re-evaluated exactly before returning); status[2N+2 .. 2N+7] are
+ *                       CTA counters and the CFL tail's running max (csrc/fvb_tail.cuh).  The
  *                       kernels leave all of them at zero, so a step loop needs no memset
  *                       (zero_status = 0).
  * Asynchronous on `stream`.  Returns FVB_OK or FVB_ERR_CONTRACT / FVB_ERR_CUDA. */
@@ -95,9 +95,10 @@ int fvb_update(const fvb_spec* spec, const double* qin, double* qout, const doub
 /* fvb_update (zero_status = 0) followed by the CFL step control of the multi-step
  * driver (no reference code): *gmax = max over the batch's max_eig
  * (NaN wins, as numpy's max), and with set_dt, dt = (cfl*dx)/gmax into *dt_scalar and
- * every dt[patch].  On the fused paths, for up to 16,384 patches, the reduction runs
- * inside the update's redo pass (one CTA), so a step is two launches and no memset;
- * otherwise the reduce kernels follow.  Asynchronous on `stream`. */
+ * every dt[patch].  On the fused paths the reduction rides on the update itself (each CTA
+ * folds its patches' max_eig into a running max, the last one writes gmax and dt_scalar)
+ * and the redo pass broadcasts dt, so a step is two launches and no memset; the generic
+ * kernel is followed by the reduce kernels.  Asynchronous on `stream`. */
 int fvb_update_cfl(const fvb_spec* spec, const double* qin, double* qout, const double* cell_size,
                    double* dt, double* max_eig, uint32_t* status, int kernel, double cfl, double dx,
                    double* gmax, double* dt_scalar, int set_dt, void* stream);
@@ -114,13 +115,13 @@ int fvb_step_record(int64_t* step, const double* dt_scalar, const uint32_t* stat
  * fvb_update_cfl / fvb_update_to_haloed call made by this host thread records the CUDA
  * event `start` (a cudaEvent_t) on its stream right before its main kernel and `stop`
  * right after it -- the exact redo pass and the reduce kernels excluded (the CFL tail
- * that runs in the main kernel's last CTA is included).  One-shot;
+ * that runs at the end of the main kernel is included).  One-shot;
  * either pointer may be NULL. */
 int fvb_time_next_update(void* start, void* stop);
 
-/* Number of uint32 status words fvb_update needs for n patches (2n + 5: flag,
+/* Number of uint32 status words fvb_update needs for n patches (2n + 8: flag,
  * redo count, redo list -- sized 2n for kernels that may queue a patch twice --
- * two CTA counters and the CFL-tail mark). */
+ * two CTA counters, two spare words and the CFL tail's 64-bit running max). */
 size_t fvb_status_words(int64_t n_patches);
 
 /* Same step from HOST arrays (the reference's calling convention, numpy

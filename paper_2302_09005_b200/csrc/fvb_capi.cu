@@ -138,7 +138,7 @@ int update_impl(const fvb_spec* spec, const double* qin, double* qout, const dou
   a.dt = dt;
   a.max_eig = max_eig;
   a.status = status;
-  const bool tail_in_redo = tail && k == FVB_KERNEL_FUSED && spec->n_patches <= kTailMaxPatches;
+  const bool tail_in_redo = tail && k == FVB_KERNEL_FUSED;   // every fused kernel carries the CFL tail
   if (tail_in_redo) {
     a.gmax = tail->gmax;
     a.cfl = tail->cfl;
@@ -194,7 +194,7 @@ int fvb_update_cfl(const fvb_spec* spec, const double* qin, double* qout, const 
   return update_impl(spec, qin, qout, cell_size, dt, max_eig, status, kernel, 0, &tail, stream);
 }
 
-static size_t status_bytes(int64_t chunk) { return ((size_t)(2 * chunk + 5) * 4 + 255) / 256 * 256; }
+static size_t status_bytes(int64_t chunk) { return ((size_t)(2 * chunk + 8) * 4 + 255) / 256 * 256; }
 static size_t align256(size_t b) { return (b + 255) / 256 * 256; }
 // One buffer set of the host pipeline: qin, qout, cell_size, dt, max_eig, each
 // 256-byte aligned (the fused kernels move patches with TMA bulk copies, which
@@ -205,7 +205,7 @@ static size_t host_set_bytes(const fvb_spec* spec, int64_t chunk) {
          align256((size_t)chunk * spec->dim * 8) + 2 * align256((size_t)chunk * 8);
 }
 
-size_t fvb_status_words(int64_t n_patches) { return (size_t)(2 * n_patches + 5); }
+size_t fvb_status_words(int64_t n_patches) { return (size_t)(2 * n_patches + 8); }
 
 size_t fvb_update_host_workspace(const fvb_spec* spec, int64_t chunk) {
   if (check_spec(spec) || chunk < 1) return 0;

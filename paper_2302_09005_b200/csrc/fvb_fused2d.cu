@@ -25,6 +25,7 @@
 #include "fvb_exact.cuh"
 #include "fvb_kernels.h"
 #include "fvb_layout.cuh"
+#include "fvb_tail.cuh"
 #include "fvb_tma.cuh"
 
 namespace fvb {
@@ -78,7 +79,7 @@ template <int L, int MINB>
 __global__ void __launch_bounds__(288, MINB)
 fused2d_kernel(const double* __restrict__ qin, double* __restrict__ qout, const double* __restrict__ cell_size,
                const double* __restrict__ dtv, double* __restrict__ max_eig, unsigned* __restrict__ status,
-               int64_t n, Closure cl) {
+               int64_t n, Closure cl, CflTail tail) {
   extern __shared__ __align__(128) double sm[];
   double* ring = sm + OFF_RING;
   double* ysb = sm + OFF_YS;
@@ -296,6 +297,15 @@ fused2d_kernel(const double* __restrict__ qin, double* __restrict__ qout, const 
     slot3 = slot3 == 2 ? 0 : slot3 + 1;
   }
 
+  if (tail.gmax) {   // fvb_update_cfl: fold the CTA's max_eig into the step's max (fvb_tail.cuh)
+    __syncthreads();   // the producer wrote them
+    unsigned long long m = 0;
+    for (int g = tid; g < G; g += 288) {
+      const unsigned long long v = (unsigned long long)__double_as_longlong(max_eig[patch_of(g)]);
+      m = v > m ? v : m;
+    }
+    fused_warp_tail(tail, status, n, m, gridDim.x * 9);
+  }
   if (producer) bulk_wait_all0();
 }
 
@@ -313,7 +323,8 @@ cudaError_t launch(const FvbArgs& a, cudaStream_t st) {
   int64_t grid = (int64_t)sms * per_sm;
   if (grid > a.n) grid = a.n;
   const Closure cl{a.gamma, a.gamma - 1.0};
-  kfn<<<(unsigned)grid, 288, BYTES, st>>>(a.qin, a.qout, a.cell_size, a.dt, a.max_eig, a.status, a.n, cl);
+  const CflTail tail{a.gmax, a.cfl, a.dx, a.dt_scalar, a.dt_patches, a.tail_dt};
+  kfn<<<(unsigned)grid, 288, BYTES, st>>>(a.qin, a.qout, a.cell_size, a.dt, a.max_eig, a.status, a.n, cl, tail);
   return cudaGetLastError();
 }
 

@@ -32,6 +32,7 @@
 #include "fvb_fast.cuh"
 #include "fvb_kernels.h"
 #include "fvb_layout.cuh"
+#include "fvb_tail.cuh"
 #include "fvb_tma.cuh"
 
 #include <cuda.h>
@@ -111,7 +112,7 @@ __global__ void __launch_bounds__(WPC * 32, 4)
 fused2d_warp_kernel(const double* __restrict__ qin, double* __restrict__ qout, const double* __restrict__ cell_size,
                     const double* __restrict__ dtv, double* __restrict__ max_eig, unsigned* __restrict__ status,
                     int64_t n, Closure cl, const __grid_constant__ CUtensorMap tmap,
-                    const __grid_constant__ CUtensorMap omap, int out_haloed) {
+                    const __grid_constant__ CUtensorMap omap, int out_haloed, CflTail tail) {
   using C = W2<P>;
   constexpr int E = C::E, PPW = C::PPW, ROWD = C::ROWD, OFFB = C::OFFB, STGD = C::STGD, NS = C::NS, HB = C::HB;
   constexpr int XSD = C::XSD, HXR = C::HXR, HXC = C::HXC, OUTR = C::OUTR, OFFO = C::OFFO;
@@ -450,6 +451,19 @@ fused2d_warp_kernel(const double* __restrict__ qin, double* __restrict__ qout, c
       }
     }
   }
+  if (tail.gmax) {   // fvb_update_cfl: fold the warp's max_eig into the step's max (fvb_tail.cuh)
+    __syncwarp();
+    unsigned long long m = 0;
+    for (int i = l; i < my_items * PPW; i += 32) {
+      const int j = i / PPW;
+      const int64_t pidx = PPW * (gw + (int64_t)j * tw) + (i - j * PPW);
+      if (pidx < n) {
+        const unsigned long long v = (unsigned long long)__double_as_longlong(max_eig[pidx]);
+        m = v > m ? v : m;
+      }
+    }
+    fused_warp_tail(tail, status, n, m, gridDim.x * WPC);
+  }
   if (l == 0) bulk_wait_all0();
 }
 
@@ -515,8 +529,9 @@ cudaError_t launch(const FvbArgs& a, cudaStream_t st) {
   e = make_qin_map<P>(a, &tm);
   if (e == cudaSuccess) e = make_qout_map<P>(a, &om);
   if (e != cudaSuccess) return e;
+  const CflTail tail{a.gmax, a.cfl, a.dx, a.dt_scalar, a.dt_patches, a.tail_dt};
   kfn<<<(unsigned)grid, WPC * 32, BYTES, st>>>(a.qin, a.qout, a.cell_size, a.dt, a.max_eig, a.status, a.n, cl, tm,
-                                               om, a.out_haloed);
+                                               om, a.out_haloed, tail);
   return cudaGetLastError();
 }
 }  // namespace f2w

@@ -178,6 +178,7 @@ fused3d_half_kernel(const double* __restrict__ qin, double* __restrict__ qout, c
     }
     bulk_commit();
   };
+  __shared__ unsigned long long tail_m;   // max of the max_eig the producer wrote (fused_kernel_tail)
   auto finish_patch = [&](int j, int64_t pidx) {   // after the patch's last row block, item j
     static_assert(IPP <= 2, "wmax / slowflag hold two items");
     unsigned long long m = 0;
@@ -194,6 +195,7 @@ fused3d_half_kernel(const double* __restrict__ qin, double* __restrict__ qout, c
       slowflag[par] = 0;
     }
     reinterpret_cast<unsigned long long*>(max_eig)[pidx] = m;
+    tail_m = m > tail_m ? m : tail_m;   // (the producer alone)
     if (slow_any) {   // queue the patch for the exact re-evaluation (fvb_redo_kernel)
       const unsigned k = atomicAdd(&status[1], 1u);
       status[2 + k] = (unsigned)pidx;
@@ -203,6 +205,7 @@ fused3d_half_kernel(const double* __restrict__ qin, double* __restrict__ qout, c
   if (producer) {
 #pragma unroll
     for (int s = 0; s < NST; ++s) mbar_init(&bars[s], 1);
+    tail_m = 0;
     slowflag[0] = slowflag[1] = 0;
     fence_mbar_init();
   }
@@ -395,7 +398,7 @@ fused3d_half_kernel(const double* __restrict__ qin, double* __restrict__ qout, c
   }
 
   if (producer) bulk_wait_all0();
-  fused_kernel_tail(tail, max_eig, status, n, producer);   // fvb_update_cfl: the step's max / dt
+  fused_kernel_tail(tail, status, n, producer ? tail_m : 0ull);   // fvb_update_cfl: the step's max / dt
 }
 
 template <int L>

@@ -22,8 +22,8 @@ struct FvbArgs {
   double* max_eig;
   unsigned* status;
   int out_haloed = 0;   // 1: qout is a haloed AoS batch (N*V*S); the update fills its interior
-  // CFL tail (fvb_update_cfl): the redo pass's last CTA (or CTA 0 when the list is
-  // empty) reduces max_eig to *gmax and, with tail_dt, writes dt = (cfl*dx)/gmax
+  // CFL tail (fvb_update_cfl, fvb_tail.cuh): the fused kernel's last CTA / warp writes
+  // *gmax (and dt_scalar) from the running max, the redo pass broadcasts dt = (cfl*dx)/gmax
   double* gmax = nullptr;
   double cfl = 0.0, dx = 0.0;
   double* dt_scalar = nullptr;
@@ -31,7 +31,6 @@ struct FvbArgs {
   int tail_dt = 0;
 };
 
-constexpr int64_t kTailMaxPatches = 16384;   // one CTA reduces max_eig within the redo pass
 
 cudaError_t fvb_launch_generic(const FvbArgs& a, cudaStream_t st);
 cudaError_t fvb_launch_step_record(int64_t* step, const double* dt_scalar, const unsigned* status,

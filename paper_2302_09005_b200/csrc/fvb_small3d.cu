@@ -22,6 +22,7 @@
 
 #include "fvb_kernels.h"
 #include "fvb_layout.cuh"
+#include "fvb_tail.cuh"
 #include "fvb_tma.cuh"
 
 namespace fvb {
@@ -118,7 +119,7 @@ template <int P, bool FAST = false>
 __global__ void __launch_bounds__(Cfg<P, FAST>::THREADS, P == 4 ? (FAST ? 8 : 6) / Cfg<P, FAST>::PPC : 1)
 small3d_kernel(const double* __restrict__ qin, double* __restrict__ qout, const double* __restrict__ cell_size,
                const double* __restrict__ dtv, double* __restrict__ max_eig, unsigned* __restrict__ status,
-               int64_t n_patches, Closure cl, const __grid_constant__ CUtensorMap omap) {
+               int64_t n_patches, Closure cl, const __grid_constant__ CUtensorMap omap, CflTail tail) {
   using C = Cfg<P, FAST>;
   constexpr int S = C::S, E = C::E;
   // Odd P: a patch is an odd multiple of 8 bytes, so neither the bulk copies nor the
@@ -466,6 +467,18 @@ small3d_kernel(const double* __restrict__ qin, double* __restrict__ qout, const 
     stg = stg == C::NST - 1 ? 0 : stg + 1;
     par ^= (stg == 0);
   }
+  if (tail.gmax) {   // fvb_update_cfl: fold the CTA's max_eig into the step's max (fvb_tail.cuh)
+    __syncthreads();   // thread 0 wrote them
+    unsigned long long m = 0;
+    for (int i = tid; i < G * C::PPC; i += C::THREADS) {
+      const int64_t pidx = group_of(i / C::PPC) * C::PPC + i % C::PPC;
+      if (pidx < n_patches) {
+        const unsigned long long v = (unsigned long long)__double_as_longlong(max_eig[pidx]);
+        m = v > m ? v : m;
+      }
+    }
+    fused_warp_tail(tail, status, n_patches, m, gridDim.x * (C::THREADS / 32));
+  }
   if (tid == 0) bulk_wait_all0();
 }
 
@@ -500,8 +513,9 @@ cudaError_t launch(const FvbArgs& a, cudaStream_t st) {
         CUDA_SUCCESS)
       return cudaErrorInvalidValue;
   }
+  const CflTail tail{a.gmax, a.cfl, a.dx, a.dt_scalar, a.dt_patches, a.tail_dt};
   kfn<<<(unsigned)grid, C::THREADS, C::BYTES, st>>>(a.qin, a.qout, a.cell_size, a.dt, a.max_eig, a.status, a.n,
-                                                    cl, omap);
+                                                    cl, omap, tail);
   return cudaGetLastError();
 }
 

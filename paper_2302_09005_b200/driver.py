@@ -53,9 +53,10 @@ class CflStepper:
     """Device-resident step loop for one shard: update -> local max wave speed ->
     (NCCL MAX all-reduce) -> dt, every step enqueued without a host synchronisation.
 
-    The redo list of the fused kernels empties itself (fvb_status_words) and the max
-    reduction + dt run inside the update's redo pass (fvb_update_cfl), so a step is two
-    kernels and no memset on one GPU for up to 16,384 patches; on N GPUs the local max,
+    The redo list of the fused kernels empties itself (fvb_status_words), the max
+    reduction rides on the update kernel (a running max its CTAs fold into; the last one
+    writes gmax and dt_scalar) and the redo pass broadcasts dt (fvb_update_cfl), so a step
+    is two kernels and no memset on one GPU for any batch size; on N GPUs the local max,
     the all-reduce and fvb_set_dt.
     graph=True captures that step once in a CUDA graph and replays it, which removes the
     per-launch host cost (ctypes + driver) from small-shard strong scaling."""

@@ -31,7 +31,7 @@ def test_library_exports_every_declared_symbol():
         assert hasattr(lib, name), name
     L = _lib.load()
     assert L.fvb_version() >= 1
-    assert L.fvb_status_words(10) == 25
+    assert L.fvb_status_words(10) == 28
 
 
 def test_capi_contract_checks_without_gpu():
