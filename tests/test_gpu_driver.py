@@ -295,14 +295,18 @@ def test_update_range_split_matches_whole(dim, p, grid, monkeypatch):
     assert_bits_equal(sg.db.max_eigenvalue.cpu().numpy(), whole.max_eigenvalue[lo:hi].cpu().numpy(), "max_eig")
 
 
-@pytest.mark.parametrize("dim,p,n,kernel,negzero", [(3, 16, 300, "auto", False), (3, 16, 40, "auto", True),
-                                                    (2, 16, 2000, "auto", False), (3, 4, 20000, "auto", False),
-                                                    (3, 7, 30, "generic", False), (2, 5, 64, "auto", True)])
+@pytest.mark.parametrize("dim,p,n,kernel,negzero,layout", [
+    (3, 16, 300, "auto", False, "aos"), (3, 16, 40, "auto", True, "aos"), (2, 16, 2000, "auto", False, "aos"),
+    (3, 4, 20000, "auto", False, "aos"), (3, 4, 20000, "auto", True, "aos"), (2, 16, 20000, "auto", True, "aos"),
+    (3, 7, 30, "generic", False, "aos"), (2, 5, 64, "auto", True, "aos"), (2, 16, 3000, "auto", True, "soa"),
+    (3, 16, 60, "auto", False, "soa")])
 @pytest.mark.parametrize("mode", ["exact", "fast"])
-def test_update_cfl_tail_matches_host(dim, p, n, kernel, negzero, mode):
+def test_update_cfl_tail_matches_host(dim, p, n, kernel, negzero, layout, mode):
     """fvb_update_cfl: QOut / max_eig as fvb_update, gmax = max(max_eig) and dt = (cfl*dx)/gmax
-    (fvb_set_dt's rounding) in every dt slot -- via the redo pass's tail (empty list: CTA 0;
-    queued patches: the last CTA), or the reduce kernels (generic kernel, > 16,384 patches)."""
+    (fvb_set_dt's rounding) in every dt slot -- via the fused kernel's running max and the redo
+    pass's broadcast (empty list), the redo pass's last CTA (queued patches), or the reduce
+    kernels (generic kernel); every fused kernel family (3D p=16 fast / half, small-patch, 2D
+    warp AoS, 2D block SoA), above and below 16,384 patches."""
     b = mesh.make_patch_batch(mesh.PatchSpec(dim, p, dim + 2), n)
     q = oracle.synthetic_qin(dim, p, n, seed=n + p).reshape(n, -1, dim + 2)
     if negzero:
@@ -311,19 +315,20 @@ def test_update_cfl_tail_matches_host(dim, p, n, kernel, negzero, mode):
     b.dt[...] = 0.4 * (1.0 / p) / 3.4
     ref_q, ref_l, st = oracle.update(dim, p, 1.4, b.QIn, b.cell_size, b.dt)
     assert st == 0
-    db = device.DeviceBatch.from_host(b, 1.4)
+    db = device.DeviceBatch.from_host(b, 1.4, layout=layout)
     gmax = torch.zeros(1, dtype=torch.float64, device="cuda")
     dts = torch.zeros(1, dtype=torch.float64, device="cuda")
-    for _ in range(2):   # twice: the redo list and its CTA counter must have reset themselves
+    for _ in range(2):   # twice: the redo list, the CTA counters and the running max reset themselves
         db.dt.fill_(b.dt[0])
         db.update_cfl(0.4, 1.0 / p, gmax, dts, kernel=kernel, mode=mode)
         torch.cuda.synchronize()
         st_words = db.status.cpu().numpy()
-        assert st_words[1] == 0 and np.all(st_words[-3:] == 0), st_words[-3:]   # list, counters, tail mark
+        assert st_words[1] == 0 and np.all(st_words[-6:] == 0), st_words[-6:]   # list, counters, running max
         out = mesh.make_patch_batch(b.spec, n)
         db.to_host(out)
         # fast kernels (3D p = 16, 2D p = 2..32, 3D p = 2, 4..8): 1e-12 parity, not bitwise
-        fast16 = mode == "fast" and kernel == "auto" and (p == 16 or dim == 2 or p in (2, 4, 5, 6, 7, 8))
+        fast16 = mode == "fast" and kernel == "auto" and layout == "aos" and (p == 16 or dim == 2 or
+                                                                              p in (2, 4, 5, 6, 7, 8))
         if not fast16:
             assert_bits_equal(out.QOut, ref_q, "QOut")
             assert_bits_equal(out.max_eigenvalue, ref_l, "max_eig")
