@@ -48,7 +48,20 @@ struct Cfg {
   static constexpr int THREADS = (PPC * IVOL + 31) / 32 * 32;   // whole warps; threads past the cells idle
   static constexpr int NHALO = 6 * P * P;           // face-halo volumes per patch
   static constexpr int LINE = E * P * P;            // records of one direction: (E along n) x P x P
-  static constexpr int STAGE = PPC * VOL * S;       // doubles per ring stage
+  // BOXED (fast p = 4): a patch is staged as two TMA tensor boxes -- the 4 interior z planes
+  // whole (6 x 6 volumes, incl. the x / y face halos) and the 4 x 4 face-halo rows of the two
+  // z-halo planes (22 doubles from byte 32 of each row: the box start must be 16-byte aligned,
+  // so the last unknown of volume 0 and the first of volume 5 come along) -- 7,168 of the
+  // patch's 8,640 bytes: the z-halo planes' edge / corner volumes are never read
+#ifndef FVB_SMALL3D_BOXES
+#define FVB_SMALL3D_BOXES 1
+#endif
+  static constexpr bool BOXED = FAST && P == 4 && FVB_SMALL3D_BOXES && PPC == 1;
+  static constexpr int BOXA = P * E * E * S;          // interior z planes, whole
+  static constexpr int ZROW = P * S + 2;              // a z-halo row's face volumes + 2 boundary doubles
+  static constexpr int BOXC = 2 * P * ZROW;
+  static constexpr int PSTAGE = BOXED ? BOXA + BOXC : VOL * S;   // doubles per staged patch
+  static constexpr int STAGE = PPC * PSTAGE;        // doubles per ring stage
   static constexpr int NST = 2;
   // exact: side data of one patch, 3 directions; FAST: (r, p, c) of every haloed volume
   static constexpr int SIDE = FAST ? VOL * 3 : 3 * S * LINE;
@@ -119,7 +132,8 @@ template <int P, bool FAST = false>
 __global__ void __launch_bounds__(Cfg<P, FAST>::THREADS, P == 4 ? (FAST ? 8 : 6) / Cfg<P, FAST>::PPC : 1)
 small3d_kernel(const double* __restrict__ qin, double* __restrict__ qout, const double* __restrict__ cell_size,
                const double* __restrict__ dtv, double* __restrict__ max_eig, unsigned* __restrict__ status,
-               int64_t n_patches, Closure cl, const __grid_constant__ CUtensorMap omap, CflTail tail) {
+               int64_t n_patches, Closure cl, const __grid_constant__ CUtensorMap omap, CflTail tail,
+               const __grid_constant__ CUtensorMap amap, const __grid_constant__ CUtensorMap cmap) {
   using C = Cfg<P, FAST>;
   constexpr int S = C::S, E = C::E;
   // Odd P: a patch is an odd multiple of 8 bytes, so neither the bulk copies nor the
@@ -144,6 +158,15 @@ small3d_kernel(const double* __restrict__ qin, double* __restrict__ qout, const 
   // (word offsets 4*hz + 5*hx mod 16 are distinct).
   const int cx = cell % P, cz = (cell / P) % P, cy = cell / (P * P);
   const int warp = tid >> 5, lane = tid & 31;
+  // stage offset (doubles) of haloed volume (hx, hy, hz) of a staged patch
+  auto soff = [&](int hx, int hy, int hz) -> int {
+    if constexpr (C::BOXED) {
+      return (hz >= 1 && hz <= P) ? ((hz - 1) * E + hy) * E * S + hx * S
+                                  : C::BOXA + ((hz > P ? P : 0) + hy - 1) * C::ZROW + (hx - 1) * S + 1;
+    } else {
+      return ((hz * E + hy) * E + hx) * S;
+    }
+  };
   constexpr int WPP = C::THREADS / 32 / C::PPC;   // warps per patch (PPC > 1 needs IVOL % 32 == 0)
   static_assert(C::PPC == 1 || C::IVOL % 32 == 0, "patch slots must own whole warps");
   const int64_t ngroups = (n_patches + C::PPC - 1) / C::PPC;
@@ -173,6 +196,10 @@ small3d_kernel(const double* __restrict__ qin, double* __restrict__ qout, const 
         tma_load_1d(dst + E * E * S, src + E * E * S, MID, bar);
         tma_load_1d(dst + ((E - 1) * E * E + E) * S, src + ((E - 1) * E * E + E) * S, ZROWS, bar);
       }
+    } else if (C::BOXED) {   // {x*S, y, z, patch} boxes: z = 1..P whole, z = 0 / P+1 face rows
+      mbar_expect_tx(bar, (uint32_t)(C::PSTAGE * 8));
+      tma_load_4d(st, &amap, 0, 0, 1, (int)grp, bar);
+      tma_load_4d(st + C::BOXA, &cmap, S - 1, 1, 0, (int)grp, bar);
     } else {
       mbar_expect_tx(bar, (uint32_t)(np * C::VOL * S * 8));
       tma_load_1d(st, qin + grp * C::PPC * (int64_t)C::VOL * S, (uint32_t)(np * C::VOL * S * 8), bar);
@@ -223,10 +250,10 @@ small3d_kernel(const double* __restrict__ qin, double* __restrict__ qout, const 
     const int64_t pidx = grp * C::PPC + lp;
     const double cs_cur = cs_next, dt_cur = dt_next;
     scalars(g + 1, cs_next, dt_next);
-    const double* st = ring + stg * C::STAGE + lp * C::VOL * S;
+    const double* st = ring + stg * C::STAGE + lp * C::PSTAGE;
     double* side = sideb + lp * C::SIDE;
     mbar_wait(&bars[stg], par);
-    auto qat = [&](int hx, int hy, int hz, int u) { return st[((hz * E + hy) * E + hx) * S + u]; };
+    auto qat = [&](int hx, int hy, int hz, int u) { return st[soff(hx, hy, hz) + u]; };
     auto load = [&](int hx, int hy, int hz, double (&q)[S]) {
 #pragma unroll
       for (int u = 0; u < S; ++u) q[u] = qat(hx, hy, hz, u);
@@ -281,10 +308,10 @@ small3d_kernel(const double* __restrict__ qin, double* __restrict__ qout, const 
       const int hx = nd == 0 ? hn : a + 1;
       const int hy = nd == 1 ? hn : (nd == 0 ? a + 1 : b + 1);
       const int hz = nd == 2 ? hn : b + 1;
-      const double* stt = ring + stg * C::STAGE + lpt * C::VOL * S;
+      const double* stt = ring + stg * C::STAGE + lpt * C::PSTAGE;
       double qh[S];
 #pragma unroll
-      for (int u = 0; u < S; ++u) qh[u] = stt[((hz * E + hy) * E + hx) * S + u];
+      for (int u = 0; u < S; ++u) qh[u] = stt[soff(hx, hy, hz) + u];
       Side<3> sh;
       bool okh = true;
       if constexpr (FAST) {
@@ -514,8 +541,28 @@ cudaError_t launch(const FvbArgs& a, cudaStream_t st) {
       return cudaErrorInvalidValue;
   }
   const CflTail tail{a.gmax, a.cfl, a.dx, a.dt_scalar, a.dt_patches, a.tail_dt};
+  CUtensorMap amap, cmap;   // BOXED: QIn as {x*S, y, z, patch}
+  memset(&amap, 0, sizeof(amap));
+  memset(&cmap, 0, sizeof(cmap));
+  if (C::BOXED) {
+    EncodeTiledFn enc = encode_tiled();
+    if (!enc) return cudaErrorNotSupported;
+    constexpr int E = C::E, S = C::S;
+    const cuuint64_t dims[4] = {(cuuint64_t)E * S, (cuuint64_t)E, (cuuint64_t)E, (cuuint64_t)a.n};
+    const cuuint64_t strides[3] = {(cuuint64_t)E * S * 8, (cuuint64_t)E * E * S * 8, (cuuint64_t)C::VOL * S * 8};
+    const cuuint32_t boxa[4] = {(cuuint32_t)(E * S), (cuuint32_t)E, (cuuint32_t)P, 1u};
+    const cuuint32_t boxc[4] = {(cuuint32_t)C::ZROW, (cuuint32_t)P, (cuuint32_t)E, 1u};
+    const cuuint32_t esa[4] = {1u, 1u, 1u, 1u}, esc[4] = {1u, 1u, (cuuint32_t)(E - 1), 1u};   // z = 0, E-1
+    if (enc(&amap, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, const_cast<double*>(a.qin), dims, strides, boxa, esa,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS ||
+        enc(&cmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, const_cast<double*>(a.qin), dims, strides, boxc, esc,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+      return cudaErrorInvalidValue;
+  }
   kfn<<<(unsigned)grid, C::THREADS, C::BYTES, st>>>(a.qin, a.qout, a.cell_size, a.dt, a.max_eig, a.status, a.n,
-                                                    cl, omap, tail);
+                                                    cl, omap, tail, amap, cmap);
   return cudaGetLastError();
 }
 
