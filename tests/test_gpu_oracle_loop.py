@@ -116,3 +116,15 @@ def test_full_size_c4_device_resident_vs_oracle():
     out_q = db.QOut.cpu().numpy().reshape(n, -1)
     assert_bits_equal(out_q, ref_q, "C4 full size QOut")
     assert_bits_equal(db.max_eigenvalue.cpu().numpy(), ref_l, "C4 full size max_eig")
+    # mode "fast" on the same batch (the small-patch kernel's boxed TMA staging, tensor-map
+    # patch coordinates up to 2^20): within the north star's 1e-12 relative max-norm
+    del out_q
+    db.update(mode="fast")
+    torch.cuda.synchronize()
+    assert not db.nonphysical()
+    out_q = db.QOut.cpu().numpy().reshape(-1, dim + 2)
+    ref5 = ref_q.reshape(-1, dim + 2)
+    err = float(np.max(np.max(np.abs(out_q - ref5), axis=0) / np.max(np.abs(ref5), axis=0)))
+    assert err <= 1e-12 and err < 1e-14, err
+    le = db.max_eigenvalue.cpu().numpy()
+    assert float(np.max(np.abs(le - ref_l) / ref_l)) < 1e-14
