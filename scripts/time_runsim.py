@@ -5,6 +5,7 @@ or with --2d on a 256^2 grid of 2D p=16 patches (65,536 patches, C2's batch).
     python scripts/time_runsim.py --sod    # Sod shock tube along x: fluid at rest (exact +0 momentum)
     --eager                                # step by step instead of replaying the captured CUDA graph
     --fast                                 # mode="fast" (the 1e-12 parity bar)
+    --classic                              # update + full halo projection (no direct path)
 """
 import sys
 import time
@@ -33,12 +34,13 @@ else:
     q[:, :, 0] += 0.1 * torch.rand(n, p ** dim, device="cuda", dtype=torch.float64)
 db.cell_size.fill_(1.0 / 16)
 mode = "fast" if "--fast" in sys.argv else "exact"
-driver.run_simulation(db, g, steps=2, graph="--eager" not in sys.argv, mode=mode)
+direct = False if "--classic" in sys.argv else None
+driver.run_simulation(db, g, steps=2, graph="--eager" not in sys.argv, mode=mode, direct=direct)
 torch.cuda.synchronize()
 graph = "--eager" not in sys.argv
 for steps in (10, 40, 200):
     t0 = time.perf_counter()
-    res = driver.run_simulation(db, g, steps=steps, graph=graph, mode=mode)
+    res = driver.run_simulation(db, g, steps=steps, graph=graph, mode=mode, direct=direct)
     torch.cuda.synchronize()
     dt = time.perf_counter() - t0
     print(f"run_simulation {dim}D {mode} {steps} steps: {dt / steps * 1e3:.3f} ms/step, "
