@@ -225,10 +225,11 @@ def oracle_steps(qin, cs, dt, dim, p, steps, warmup, budget_s):
     oracle.update(dim, p, 1.4, qin[:probe], cs[:probe], dt[:probe], nthreads=cores)
     per_patch = (time.perf_counter() - t0) / probe
     m = int(max(1, min(n, budget_s / max(steps + warmup, 1) / per_patch)))
+    slices = max(1, n // m)   # every step a full m-patch slice (a ragged tail slice would time mostly overhead)
     rates, ms = [], []
     for k in range(warmup + steps):
-        lo = (k * m) % n
-        hi = min(n, lo + m)
+        lo = (k % slices) * m
+        hi = lo + m
         t0 = time.perf_counter()
         oracle.update(dim, p, 1.4, qin[lo:hi], cs[lo:hi], dt[lo:hi], nthreads=cores)
         el = time.perf_counter() - t0
