@@ -19,6 +19,28 @@ def test_reference_arm_json_line():
     assert line["impl"] == "reference" and line["value"] > 0
     assert line["cpu_baseline"]["kind"] == "port" and line["cpu_baseline"]["cores"] >= 1
     assert line["e2e"]["h2d_bytes_per_step"] == 0 and line["config"]["workload"].startswith("3D Euler p=16")
+    ref = line.get("cpu_baseline_numpy")
+    if ref and "value" in ref:   # the reference package is installed (baseline/_ref): both engine variants
+        assert ref["kind"] == "reference" and ref["cores"] >= 1 and ref["value"] > 0
+        assert ref["unshimmed_seq"]["cores"] == 1 and ref["unshimmed_seq"]["value"] > 0
+
+
+def test_oracle_steps_time_full_slices():
+    """The CPU baseline times full m-patch slices only (no ragged tail slice)."""
+    import importlib.util
+
+    import numpy as np
+
+    import oracle
+
+    spec = importlib.util.spec_from_file_location("bench", os.path.join(ROOT, "bench.py"))
+    b = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(b)
+    n = 10
+    q = oracle.synthetic_qin(2, 4, n, seed=5)
+    rates, cores, m, ms = b.oracle_steps(q, np.ones((n, 2)), np.full(n, 0.01), 2, 4, steps=7, warmup=1,
+                                         budget_s=1e-9)
+    assert m == 1 and len(rates) == 7 and all(r > 0 for r in rates)
 
 
 def test_reference_arm_nonzero_rank_exits_quietly():
