@@ -561,12 +561,13 @@ def main():
     del host
 
     if rank == 0:
-        # fvb_update_cfl: the update kernel, its redo pass carrying the max reduction (and on
-        # one GPU the dt) for <= 16,384 patches; else a grid reduce (+ set_dt); N GPUs: set_dt
-        if kernel_name == "fused" and n <= 16384:
+        # fvb_update_cfl: the fused kernel (its CTAs fold max_eig into the running max) and its
+        # redo pass (the dt broadcast on one GPU); the generic kernel is followed by one reduce
+        # kernel (<= 16,384 patches) or a grid reduce (+ set_dt on one GPU); N GPUs: + set_dt
+        if kernel_name == "fused":
             launches_per_step = 2 + (1 if world > 1 else 0)
         else:
-            launches_per_step = (2 if kernel_name == "fused" else 1) + 2
+            launches_per_step = 1 + (1 if n <= 16384 or world > 1 else 2) + (1 if world > 1 else 0)
         line = {
             "metric": METRIC, "value": value, "unit": "cell updates/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": args.scaling,
