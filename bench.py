@@ -374,9 +374,17 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # FVB_BENCH_DIST=gloo: a functional check of the multi-rank bench on fewer GPUs than ranks
+    # (ranks share devices; NCCL refuses that) -- its timings are not scaling numbers
+    backend = os.environ.get("FVB_BENCH_DIST", "nccl")
+    if backend != "nccl":
+        local %= torch.cuda.device_count()
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
 
     dim, p, n, cfg_idx = CONFIGS[args.config]
     if args.patches:

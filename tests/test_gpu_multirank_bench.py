@@ -1,0 +1,33 @@
+"""bench.py's N > 1 path (torchrun, one process per rank, the CflStepper's MAX all-reduce,
+max-over-ranks timing, rank 0 printing the contract line) run end to end on the one GPU this
+pool has: two ranks share it through the gloo backend (FVB_BENCH_DIST=gloo; NCCL refuses two
+ranks on one device).  A functional check -- the numbers are not scaling measurements."""
+
+import json
+import os
+import subprocess
+import sys
+
+import pytest
+
+from conftest import ROOT
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():  # pragma: no cover
+    pytest.skip("no CUDA device", allow_module_level=True)
+
+
+def test_bench_two_ranks_gloo():
+    env = dict(os.environ, FVB_BENCH_DIST="gloo")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+           "--master-addr", "127.0.0.1", "--master-port", "29517", os.path.join(ROOT, "bench.py"),
+           "--gpus", "2", "--steps", "4", "--warmup", "3", "--e2e-steps", "1", "--no-exact-leg", "--config", "c2"]
+    out = subprocess.run(cmd, capture_output=True, text=True, env=env, timeout=600, cwd=ROOT)
+    assert out.returncode == 0, out.stderr[-2000:]
+    lines = [ln for ln in out.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, out.stdout[-2000:]        # rank 0 alone prints
+    line = json.loads(lines[0])
+    assert line["n_gpus"] == 2 and line["scaling"] == "weak" and line["value"] > 0
+    assert line["gpu_launches"] == 4 * 3                # update, redo pass, set_dt per step on N > 1
+    assert line["e2e"]["value"] > 0 and line["roofline"]["kernel_ms"] > 0
