@@ -62,7 +62,7 @@ class CflStepper:
     per-launch host cost (ctypes + driver) from small-shard strong scaling."""
 
     def __init__(self, db: DeviceBatch, cfl: float = 0.4, dx: float | None = None, group=None,
-                 kernel="auto", stream=None, mode: str = "exact", graph: bool = False):
+                 kernel="auto", stream=None, mode: str = "exact", graph: bool = False, local: bool = False):
         torch = _torch()
         self.db = db
         self.cfl = float(cfl)
@@ -77,7 +77,8 @@ class CflStepper:
         self.dt_scalar = torch.zeros(1, dtype=torch.float64, device=db.device)
         import torch.distributed as dist
 
-        self._dist = dist if (dist.is_available() and dist.is_initialized()) else None
+        # local: this batch is the whole problem (run_simulation), even inside a multi-rank job
+        self._dist = dist if (not local and dist.is_available() and dist.is_initialized()) else None
 
     def _multi(self) -> bool:
         return self._dist is not None and self._dist.get_world_size(self.group) > 1
@@ -251,7 +252,7 @@ def run_simulation(db: DeviceBatch, grid_shape, steps: int, cfl: float = 0.4, pe
     init = db.QOut.clone() if diagnose and steps > 0 else None   # replayed on the error path only
     db.halo_project_totals(grid_shape, periodic, tot_h[0], scratch)
     db.status.zero_()
-    stepper = CflStepper(db, cfl=cfl, dx=dx, kernel=kernel)
+    stepper = CflStepper(db, cfl=cfl, dx=dx, kernel=kernel, local=True)
     stepper.prepass()
     gmax_h[0].copy_(stepper.gmax[0])
     dt_h[0].copy_(stepper.dt_scalar[0])
@@ -423,16 +424,41 @@ def exchange_ghost_layers_start(own, layer_elems: int, ghost_lo, ghost_hi, rank:
         return []
     import torch.distributed as dist
 
+    # a backend without device point-to-point (gloo) moves device layers through host copies;
+    # the returned waits then also copy the received layers to the device ghosts
+    staged = own.is_cuda and dist.get_backend(group) != "nccl"
+    send_last = last.cpu() if staged else last.contiguous()
+    send_first = first.cpu() if staged else first.contiguous()
+    recv_lo = torch_empty_like_host(ghost_lo) if (staged and lo is not None) else ghost_lo
+    recv_hi = torch_empty_like_host(ghost_hi) if (staged and hi is not None) else ghost_hi
     ops = []
     if hi is not None:
-        ops.append(dist.P2POp(dist.isend, last.contiguous(), hi, group))
+        ops.append(dist.P2POp(dist.isend, send_last, hi, group))
     if lo is not None:
-        ops.append(dist.P2POp(dist.isend, first.contiguous(), lo, group))
+        ops.append(dist.P2POp(dist.isend, send_first, lo, group))
     if lo is not None:
-        ops.append(dist.P2POp(dist.irecv, ghost_lo, lo, group))
+        ops.append(dist.P2POp(dist.irecv, recv_lo, lo, group))
     if hi is not None:
-        ops.append(dist.P2POp(dist.irecv, ghost_hi, hi, group))
-    return dist.batch_isend_irecv(ops)   # the caller waits (after overlapping work, if any)
+        ops.append(dist.P2POp(dist.irecv, recv_hi, hi, group))
+    works = dist.batch_isend_irecv(ops)   # the caller waits (after overlapping work, if any)
+    if not staged:
+        return works
+
+    class _StagedWait:
+        def wait(self_):
+            for w in works:
+                w.wait()
+            if lo is not None:
+                ghost_lo.copy_(recv_lo)
+            if hi is not None:
+                ghost_hi.copy_(recv_hi)
+
+    return [_StagedWait()]
+
+
+def torch_empty_like_host(t):
+    """A host tensor shaped like device tensor t (the staging buffer of a gloo exchange)."""
+    return _torch().empty(t.shape, dtype=t.dtype)
 
 
 def shard_layout(grid_shape, rank: int, world: int, periodic: bool) -> dict:

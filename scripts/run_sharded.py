@@ -50,9 +50,15 @@ def main():
     a = ap.parse_args()
     grid = tuple(int(g) for g in a.grid.split(","))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    backend = os.environ.get("FVB_BENCH_DIST", "nccl")   # gloo: ranks may share a GPU (functional check)
+    if backend != "nccl":
+        local %= torch.cuda.device_count()
     torch.cuda.set_device(local)
     if int(os.environ.get("WORLD_SIZE", "1")) > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     spec = mesh.PatchSpec(a.dim, a.p, a.dim + 2)
     field = initial_field(a.dim, a.p, grid)
     sg = driver.ShardedGrid(spec, grid, 1.4, periodic=not a.aperiodic)
