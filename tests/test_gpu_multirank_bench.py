@@ -21,17 +21,19 @@ if not torch.cuda.is_available():  # pragma: no cover
     pytest.skip("no CUDA device", allow_module_level=True)
 
 
-def test_bench_two_ranks_gloo():
+@pytest.mark.parametrize("scaling", ["weak", "strong"])
+def test_bench_two_ranks_gloo(scaling):
     env = dict(os.environ, FVB_BENCH_DIST="gloo")
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
-           "--master-addr", "127.0.0.1", "--master-port", "29517", os.path.join(ROOT, "bench.py"),
-           "--gpus", "2", "--steps", "4", "--warmup", "3", "--e2e-steps", "1", "--no-exact-leg", "--config", "c2"]
+           "--master-addr", "127.0.0.1", "--master-port", "29517" if scaling == "weak" else "29518",
+           os.path.join(ROOT, "bench.py"), "--gpus", "2", "--steps", "4", "--warmup", "3", "--e2e-steps", "1",
+           "--no-exact-leg", "--config", "c2", "--scaling", scaling]
     out = subprocess.run(cmd, capture_output=True, text=True, env=env, timeout=600, cwd=ROOT)
     assert out.returncode == 0, out.stderr[-2000:]
     lines = [ln for ln in out.stdout.splitlines() if ln.startswith("{")]
     assert len(lines) == 1, out.stdout[-2000:]        # rank 0 alone prints
     line = json.loads(lines[0])
-    assert line["n_gpus"] == 2 and line["scaling"] == "weak" and line["value"] > 0
+    assert line["n_gpus"] == 2 and line["scaling"] == scaling and line["value"] > 0
     assert line["gpu_launches"] == 4 * 3                # update, redo pass, set_dt per step on N > 1
     assert line["e2e"]["value"] > 0 and line["roofline"]["kernel_ms"] > 0
 
