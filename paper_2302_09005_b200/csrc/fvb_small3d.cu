@@ -62,7 +62,10 @@ struct Cfg {
   static constexpr int BOXC = 2 * P * ZROW;
   static constexpr int PSTAGE = BOXED ? BOXA + BOXC : VOL * S;   // doubles per staged patch
   static constexpr int STAGE = PPC * PSTAGE;        // doubles per ring stage
-  static constexpr int NST = 2;
+#ifndef FVB_SMALL3D_NST8
+#define FVB_SMALL3D_NST8 3
+#endif
+  static constexpr int NST = FAST && P >= 8 ? FVB_SMALL3D_NST8 : 2;   // fast p = 8: a third stage, 754.8 vs 768 us (x3p8)
   // exact: side data of one patch, 3 directions; FAST: (r, p, c) of every haloed volume
   static constexpr int SIDE = FAST ? VOL * 3 : 3 * S * LINE;
   static constexpr int OUTN = (PPC * IVOL * S + 15) / 16 * 16;   // staging buffers 128-byte aligned (TMA)
