@@ -365,3 +365,57 @@ def test_fast_small3d_golden_and_errors():
         assert np.array_equal(np.isfinite(b.QOut), fin), case["name"]
         assert rel_maxnorm(np.where(fin, b.QOut, 0.0), np.where(fin, gold.QOut, 0.0), 5) <= TOL, case["name"]
         assert_max_eig_close(b.max_eigenvalue, gold.max_eigenvalue, case["name"])
+
+
+@pytest.mark.parametrize("dim,p", [(3, 16), (2, 16), (3, 4), (2, 7)])
+def test_fast_gate_edges(dim, p):
+    """The fast gate (c^2 = gamma p / rho positive, normal, finite; fvb_fast.cuh) at its lower
+    edge: patches whose states have c^2 ~ 1e-289 stay on the fast path (within the 1e-12 bar,
+    all intermediates still normal), patches with c^2 ~ 1e-296 go through the exact redo pass
+    (bit for bit); both kinds mixed in one batch, every fast kernel family."""
+    n = 12
+    v = (p + 2) ** dim
+    rng = np.random.default_rng(90 + p + dim)
+    b = mesh.make_patch_batch(mesh.PatchSpec(dim, p, dim + 2), n)
+    q = b.QIn.reshape(n, v, dim + 2)
+    rho = rng.uniform(0.5, 2.0, (n, v))
+    # pressure scale per patch: even patches c^2 ~ 1e-289 (fast), odd ones ~ 1e-296 (redo)
+    pscale = np.where(np.arange(n) % 2 == 0, 1e-289, 1e-296)[:, None]
+    pr = rng.uniform(0.5, 2.0, (n, v)) * pscale
+    vel = rng.uniform(-1.0, 1.0, (n, v, dim)) * np.sqrt(pscale)[..., None]
+    q[..., 0] = rho
+    q[..., 1:1 + dim] = rho[..., None] * vel
+    q[..., dim + 1] = pr / 0.4 + 0.5 * rho * np.sum(vel * vel, axis=-1)
+    b.dt[...] = 0.4 * (1.0 / p) / (3.4 * np.sqrt(pscale[:, 0]))   # a CFL-sized step at that wave speed
+    ref_q, ref_l, st = oracle.update(dim, p, 1.4, b.QIn, b.cell_size, b.dt)
+    assert st == 0
+    db, out = _fast_device(b)
+    assert not db.nonphysical()
+    s = dim + 2
+    for k in range(n):
+        if k % 2:   # redone exactly
+            assert_bits_equal(out.QOut[k], ref_q[k], f"redo patch {k}")
+            assert_bits_equal(out.max_eigenvalue[k:k + 1], ref_l[k:k + 1], f"redo patch {k} max_eig")
+        else:
+            err = rel_maxnorm(out.QOut[k], ref_q[k], s)
+            assert err <= TOL and err < 1e-14, (k, err)
+    assert_max_eig_close(out.max_eigenvalue, ref_l)
+
+
+@pytest.mark.parametrize("dim,p", [(3, 16), (2, 16), (3, 4)])
+def test_fast_negative_density_and_energy_flagged(dim, p):
+    """A volume with rho < 0 AND E < 0 has p < 0 too, so c^2 = gamma p / rho > 0: the fast
+    gate must still send its patch to the exact pass, which raises the non-physical flag as
+    the reference does (rho <= 0, pde.py:36-38)."""
+    n = 5
+    b = _batch(n, 17, p=p, vary=False, dim=dim)
+    v = (p + 2) ** dim
+    q = b.QIn.reshape(n, v, dim + 2)
+    e = p + 2
+    centre = (e // 2) * (e * e if dim == 3 else e) + (e // 2) * e + e // 2 if dim == 3 else (e // 2) * e + e // 2
+    q[2, centre, 0] = -1.0
+    q[2, centre, dim + 1] = -3.0
+    ref_q, ref_l, st = oracle.update(dim, p, 1.4, b.QIn, b.cell_size, b.dt)
+    assert st != 0
+    db, _ = _fast_device(b)
+    assert db.nonphysical()
