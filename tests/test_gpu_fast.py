@@ -419,3 +419,32 @@ def test_fast_negative_density_and_energy_flagged(dim, p):
     assert st != 0
     db, _ = _fast_device(b)
     assert db.nonphysical()
+
+
+@pytest.mark.parametrize("dim,p", [(3, 16), (2, 16), (3, 4)])
+def test_fast_gate_upper_edges(dim, p):
+    """Large scales stay within the bar on the fast path: densities ~1e80 and ~1e100, sound
+    speeds with c^2 ~ 1e190 (every flux product of both operation orders stays finite)."""
+    n = 9
+    v = (p + 2) ** dim
+    rng = np.random.default_rng(70 + p + dim)
+    b = mesh.make_patch_batch(mesh.PatchSpec(dim, p, dim + 2), n)
+    q = b.QIn.reshape(n, v, dim + 2)
+    kind = np.arange(n) % 3                      # 0: fast (rho ~ 1e80), 1: huge rho, 2: huge c^2
+    rs = np.array([1e80, 1e100, 1.0])[kind][:, None]
+    cs2 = np.array([1.0, 1.0, 1e190])[kind][:, None]
+    rho = rng.uniform(0.5, 2.0, (n, v)) * rs
+    pr = rng.uniform(0.5, 2.0, (n, v)) * rs * cs2
+    vel = rng.uniform(-1.0, 1.0, (n, v, dim)) * np.sqrt(cs2)[..., None]
+    q[..., 0] = rho
+    q[..., 1:1 + dim] = rho[..., None] * vel
+    q[..., dim + 1] = pr / 0.4 + 0.5 * rho * np.sum(vel * vel, axis=-1)
+    b.dt[...] = 0.4 * (1.0 / p) / (3.4 * np.sqrt(cs2[:, 0]))
+    ref_q, ref_l, st = oracle.update(dim, p, 1.4, b.QIn, b.cell_size, b.dt)
+    assert st == 0
+    db, out = _fast_device(b)
+    assert not db.nonphysical()
+    for k in range(n):
+        err = rel_maxnorm(out.QOut[k], ref_q[k], dim + 2)
+        assert err <= TOL and err < 1e-14, (k, kind[k], err)
+    assert_max_eig_close(out.max_eigenvalue, ref_l)
