@@ -479,3 +479,34 @@ def test_fast_high_mach_within_bar(mach):
         assert err <= TOL, (k, err)
     rel = np.max(np.abs(out.max_eigenvalue - ref_l) / ref_l)
     assert rel <= TOL, rel
+
+
+@pytest.mark.parametrize("dim,p,decades", [(3, 16, 6), (2, 16, 6), (3, 4, 6), (3, 16, 12)])
+def test_fast_strong_contrasts_within_bar(dim, p, decades):
+    """Density and pressure varying over +-`decades` decades from volume to volume inside a
+    patch (shock-like jumps at every face), velocities up to a few sound speeds: every patch
+    within the bar (relative max-norm per unknown) of the reference."""
+    n = 6
+    v = (p + 2) ** dim
+    rng = np.random.default_rng(300 + decades + p + dim)
+    b = mesh.make_patch_batch(mesh.PatchSpec(dim, p, dim + 2), n)
+    q = b.QIn.reshape(n, v, dim + 2)
+    rho = 10.0 ** rng.uniform(-decades, decades, (n, v))
+    pr = 10.0 ** rng.uniform(-decades, decades, (n, v))
+    c = np.sqrt(1.4 * pr / rho)
+    vel = rng.uniform(-3.0, 3.0, (n, v, dim)) * c[..., None]
+    q[..., 0] = rho
+    q[..., 1:1 + dim] = rho[..., None] * vel
+    q[..., dim + 1] = pr / 0.4 + 0.5 * rho * np.sum(vel * vel, axis=-1)
+    cmax = np.max(4.0 * c, axis=1)
+    b.dt[...] = 0.4 * (1.0 / p) / cmax
+    ref_q, ref_l, st = oracle.update(dim, p, 1.4, b.QIn, b.cell_size, b.dt)
+    db, out = _fast_device(b)
+    assert db.nonphysical() == (st != 0)
+    if st != 0:
+        return
+    for k in range(n):
+        err = rel_maxnorm(out.QOut[k], ref_q[k], dim + 2)
+        assert err <= TOL, (k, err)
+    rel = np.max(np.abs(out.max_eigenvalue - ref_l) / ref_l)
+    assert rel <= TOL, rel
