@@ -510,3 +510,32 @@ def test_fast_strong_contrasts_within_bar(dim, p, decades):
         assert err <= TOL, (k, err)
     rel = np.max(np.abs(out.max_eigenvalue - ref_l) / ref_l)
     assert rel <= TOL, rel
+
+
+@pytest.mark.parametrize("dim,p", [(3, 16), (2, 16), (3, 4), (2, 17), (3, 9)])
+def test_exact_strong_contrasts_bitwise(dim, p):
+    """The same 12-decade contrasts in mode "exact": bit for bit (range gates and the redo pass
+    cover whatever the fast quotient paths cannot)."""
+    n = 4
+    v = (p + 2) ** dim
+    rng = np.random.default_rng(500 + p + dim)
+    b = mesh.make_patch_batch(mesh.PatchSpec(dim, p, dim + 2), n)
+    q = b.QIn.reshape(n, v, dim + 2)
+    rho = 10.0 ** rng.uniform(-12, 12, (n, v))
+    pr = 10.0 ** rng.uniform(-12, 12, (n, v))
+    c = np.sqrt(1.4 * pr / rho)
+    vel = rng.uniform(-3.0, 3.0, (n, v, dim)) * c[..., None]
+    q[..., 0] = rho
+    q[..., 1:1 + dim] = rho[..., None] * vel
+    q[..., dim + 1] = pr / 0.4 + 0.5 * rho * np.sum(vel * vel, axis=-1)
+    b.dt[...] = 0.4 * (1.0 / p) / np.max(4.0 * c, axis=1)
+    ref_q, ref_l, st = oracle.update(dim, p, 1.4, b.QIn, b.cell_size, b.dt)
+    db = device.DeviceBatch.from_host(b, 1.4)
+    db.update(mode="exact")
+    assert db.nonphysical() == (st != 0)
+    if st != 0:
+        return
+    out = mesh.make_patch_batch(b.spec, n)
+    db.to_host(out)
+    assert_bits_equal(out.QOut, ref_q, "QOut")
+    assert_bits_equal(out.max_eigenvalue, ref_l, "max_eig")
