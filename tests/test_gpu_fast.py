@@ -539,3 +539,28 @@ def test_exact_strong_contrasts_bitwise(dim, p):
     db.to_host(out)
     assert_bits_equal(out.QOut, ref_q, "QOut")
     assert_bits_equal(out.max_eigenvalue, ref_l, "max_eig")
+
+
+@pytest.mark.parametrize("dim,p", [(3, 16), (2, 16), (3, 4)])
+@pytest.mark.parametrize("where", ["face_halo", "corner"])
+def test_fast_negative_state_in_halo(dim, p, where):
+    """rho < 0 and E < 0 in a face-halo volume (read by the reference's face boxes: flagged) or
+    in an edge / corner volume (never read: no flag, results unchanged)."""
+    n = 3
+    b = _batch(n, 23, p=p, vary=False, dim=dim)
+    e = p + 2
+    v = e ** dim
+    q = b.QIn.reshape(n, v, dim + 2)
+    mid = e // 2
+    if dim == 3:
+        vol = (mid * e + mid) * e + 0 if where == "face_halo" else (0 * e + 0) * e + 0   # x-face halo / corner
+    else:
+        vol = mid * e + 0 if where == "face_halo" else 0
+    q[1, vol, 0] = -1.0
+    q[1, vol, dim + 1] = -3.0
+    ref_q, ref_l, st = oracle.update(dim, p, 1.4, b.QIn, b.cell_size, b.dt)
+    db, out = _fast_device(b)
+    assert db.nonphysical() == (st != 0), (where, st)
+    if st == 0:
+        err = rel_maxnorm(out.QOut, ref_q, dim + 2)
+        assert err <= TOL, err
