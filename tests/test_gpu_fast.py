@@ -368,7 +368,8 @@ def test_fast_small3d_golden_and_errors():
         assert_max_eig_close(b.max_eigenvalue, gold.max_eigenvalue, case["name"])
 
 
-@pytest.mark.parametrize("dim,p", [(3, 16), (2, 16), (3, 4), (2, 7)])
+@pytest.mark.parametrize("dim,p", [(3, 16), (2, 16), (3, 4), (2, 7), (2, 2), (2, 17), (2, 32), (3, 2), (3, 5),
+                                   (3, 6), (3, 7), (3, 8)])
 def test_fast_gate_edges(dim, p):
     """The fast gate (c^2 = gamma p / rho positive, normal, finite; fvb_fast.cuh) at its lower
     edge: patches whose states have c^2 ~ 1e-289 stay on the fast path (within the 1e-12 bar,
@@ -403,7 +404,7 @@ def test_fast_gate_edges(dim, p):
     assert_max_eig_close(out.max_eigenvalue, ref_l)
 
 
-@pytest.mark.parametrize("dim,p", [(3, 16), (2, 16), (3, 4)])
+@pytest.mark.parametrize("dim,p", [(3, 16), (2, 16), (3, 4), (2, 5), (2, 31), (3, 7), (3, 8)])
 def test_fast_negative_density_and_energy_flagged(dim, p):
     """A volume with rho < 0 AND E < 0 has p < 0 too, so c^2 = gamma p / rho > 0: the fast
     gate must still send its patch to the exact pass, which raises the non-physical flag as
