@@ -568,3 +568,28 @@ def test_fast_negative_state_in_halo(dim, p, where):
     if st == 0:
         err = rel_maxnorm(out.QOut, ref_q, dim + 2)
         assert err <= TOL, err
+
+
+@pytest.mark.parametrize("mach", [1e5, 1e7])
+def test_fast3d_high_mach_halo_volume(mach):
+    """The 3D p=16 kernel tests E/p on its own volumes only (the halo warp skips it): a face-halo
+    volume at extreme Mach next to an ordinary interior must still leave the patch within the
+    bar -- its pressure's rounding enters only beside momentum / energy fluxes and a wave speed
+    that are Mach-times larger."""
+    dim, p, n = 3, 16, 4
+    b = _batch(n, 29, p=p, vary=False, dim=dim)
+    e = p + 2
+    q = b.QIn.reshape(n, e ** dim, dim + 2)
+    for vol in ((5 * e + 7) * e + 0, (9 * e + 0) * e + 4, (0 * e + 8) * e + 8):   # x-, y-, z-face halos
+        rho, pr = 1.3, 0.9
+        vel = np.array([mach, -0.5 * mach, 0.25 * mach])
+        q[1, vol] = [rho, *(rho * vel), pr / 0.4 + 0.5 * rho * vel @ vel]
+    b.dt[...] = 0.4 * (1.0 / p) / (3.4 * mach)
+    ref_q, ref_l, st = oracle.update(dim, p, 1.4, b.QIn, b.cell_size, b.dt)
+    db, out = _fast_device(b)
+    assert db.nonphysical() == (st != 0)
+    if st != 0:
+        return
+    for k in range(n):
+        err = rel_maxnorm(out.QOut[k], ref_q[k], dim + 2)
+        assert err <= TOL, (k, err)
