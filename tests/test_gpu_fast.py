@@ -593,3 +593,34 @@ def test_fast3d_high_mach_halo_volume(mach):
     for k in range(n):
         err = rel_maxnorm(out.QOut[k], ref_q[k], dim + 2)
         assert err <= TOL, (k, err)
+
+
+@pytest.mark.parametrize("dim,p", [(3, 16), (2, 16), (3, 4), (2, 17), (3, 6), (3, 9)])
+@pytest.mark.parametrize("scale", [1e-289, 1e-296, 1e100, 1e150])
+def test_exact_extreme_scales_bitwise(dim, p, scale):
+    """Mode "exact" at extreme pressure / density scales (the fast gate's edges and beyond, and
+    huge densities): bit for bit with the reference, whichever internal path (fused fast
+    quotients, range-gated slow paths, redo pass) each volume takes."""
+    n = 4
+    v = (p + 2) ** dim
+    rng = np.random.default_rng(int(np.log10(scale)) % 97 + p)
+    b = mesh.make_patch_batch(mesh.PatchSpec(dim, p, dim + 2), n)
+    q = b.QIn.reshape(n, v, dim + 2)
+    big = scale > 1.0
+    rho = rng.uniform(0.5, 2.0, (n, v)) * (scale if big else 1.0)
+    pr = rng.uniform(0.5, 2.0, (n, v)) * scale
+    vel = rng.uniform(-1.0, 1.0, (n, v, dim)) * (1.0 if big else np.sqrt(scale))
+    q[..., 0] = rho
+    q[..., 1:1 + dim] = rho[..., None] * vel
+    q[..., dim + 1] = pr / 0.4 + 0.5 * rho * np.sum(vel * vel, axis=-1)
+    b.dt[...] = 0.4 * (1.0 / p) / (3.4 * (1.0 if big else np.sqrt(scale)))
+    ref_q, ref_l, st = oracle.update(dim, p, 1.4, b.QIn, b.cell_size, b.dt)
+    db = device.DeviceBatch.from_host(b, 1.4)
+    db.update(mode="exact")
+    assert db.nonphysical() == (st != 0)
+    if st != 0:
+        return
+    out = mesh.make_patch_batch(b.spec, n)
+    db.to_host(out)
+    assert_bits_equal(out.QOut, ref_q, "QOut")
+    assert_bits_equal(out.max_eigenvalue, ref_l, "max_eig")
