@@ -624,3 +624,33 @@ def test_exact_extreme_scales_bitwise(dim, p, scale):
     db.to_host(out)
     assert_bits_equal(out.QOut, ref_q, "QOut")
     assert_bits_equal(out.max_eigenvalue, ref_l, "max_eig")
+
+
+@pytest.mark.parametrize("dim,p,chunk", [(3, 16, 3), (2, 16, 7), (3, 4, 5)])
+def test_fast_host_pipeline_with_redone_patches(dim, p, chunk):
+    """The drop-in host path (chunked H2D -> fast kernel -> redo pass -> D2H, per-chunk status
+    words) with patches that leave the fast gate in several chunks: redone ones bit for bit,
+    the rest within the bar."""
+    n = 16
+    v = (p + 2) ** dim
+    rng = np.random.default_rng(61 + p + chunk)
+    b = mesh.make_patch_batch(mesh.PatchSpec(dim, p, dim + 2), n)
+    q = b.QIn.reshape(n, v, dim + 2)
+    tiny = np.arange(n) % 3 == 1
+    pscale = np.where(tiny, 1e-296, 1.0)[:, None]
+    rho = rng.uniform(0.5, 2.0, (n, v))
+    pr = rng.uniform(0.5, 2.0, (n, v)) * pscale
+    vel = rng.uniform(-1.0, 1.0, (n, v, dim)) * np.sqrt(pscale)[..., None]
+    q[..., 0] = rho
+    q[..., 1:1 + dim] = rho[..., None] * vel
+    q[..., dim + 1] = pr / 0.4 + 0.5 * rho * np.sum(vel * vel, axis=-1)
+    b.dt[...] = 0.4 * (1.0 / p) / (3.4 * np.sqrt(pscale[:, 0]))
+    ref_q, ref_l, st = oracle.update(dim, p, 1.4, b.QIn, b.cell_size, b.dt)
+    assert st == 0
+    update_patch_batch(b, pde.make_euler_pde(dim), PW, mode="fast", chunk_patches=chunk)
+    for k in range(n):
+        if tiny[k]:
+            assert_bits_equal(b.QOut[k], ref_q[k], f"redo patch {k}")
+        else:
+            assert rel_maxnorm(b.QOut[k], ref_q[k], dim + 2) <= TOL, k
+    assert_max_eig_close(b.max_eigenvalue, ref_l)
